@@ -1,0 +1,352 @@
+/*
+ * spray_b200.h — C-ABI of the B200-native slice-spraying data plane.
+ *
+ * Two entry surfaces, both plain C (no C++ types, no torch types, no exceptions):
+ *
+ *  1. ENGINE (fused mode). The application-facing declarative intent API of the
+ *     reference `spray::Engine` (proj/include/spray/engine.hpp:90-131), with slice
+ *     decomposition, rail choice, copy execution, completion accounting and
+ *     self-healing all running inside one persistent sm_100a kernel per GPU.
+ *
+ *  2. BACKEND (plugin mode). The reference's fabric plugin boundary
+ *     `spray::TransportBackend` (proj/include/spray/backend.hpp:49-72): a CUDA
+ *     transport the reference engine would instantiate by name in
+ *     `Engine::load_backends` (proj/src/engine.cpp:116-140) and drive slice by slice.
+ *
+ * plus the replay entry used for slice-plan parity (the device decision function run
+ * over a recorded telemetry trace, proj/src/scheduler.cpp:138-230 semantics).
+ *
+ * Error model (reference: proj/include/spray/common.hpp:31-41, engine.hpp:28-31,
+ * orchestrator.hpp:20-23): API-contract violations return a negative SPRAY_E* code
+ * naming the reference exception class; `spray_last_error()` holds the message
+ * (thread-local). Datapath faults never produce an error code: they surface only as
+ * batch state, exactly like the reference.
+ */
+#ifndef SPRAY_B200_H
+#define SPRAY_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SPRAY_ABI_VERSION 1u
+
+/* ------------------------------------------------------------------ errors */
+enum spray_status {
+  SPRAY_OK = 0,
+  SPRAY_ECONFIG = -1,       /* spray::ConfigError        (common.hpp:33-36) */
+  SPRAY_EENGINE = -2,       /* spray::EngineError        (common.hpp:38-41) */
+  SPRAY_EINVALID_RANGE = -3,/* spray::InvalidRangeError  (engine.hpp:28-31) */
+  SPRAY_ENOROUTE = -4,      /* spray::NoRouteError       (orchestrator.hpp:20-23) */
+  SPRAY_ECUDA = -5,         /* CUDA runtime failure (no reference analogue; never a fallback) */
+  SPRAY_EFATAL = -6,        /* PostResult.fatal (backend.hpp:44-47): backend latched fatal */
+  SPRAY_ECAPABILITY = -7    /* capability mismatch: a programming error (backend.hpp:56-57) */
+};
+
+/* Message of the last failing call on this thread ("" when none). */
+const char* spray_last_error(void);
+uint32_t spray_abi_version(void);
+
+/* ------------------------------------------------------------------ enums */
+/* spray::Direction (common.hpp:27) */
+enum spray_direction { SPRAY_READ = 0, SPRAY_WRITE = 1 };
+/* spray::Medium (common.hpp:29). DEVICE is real HBM here, not emulated. */
+enum spray_medium { SPRAY_MEDIUM_HOST = 0, SPRAY_MEDIUM_DEVICE = 1, SPRAY_MEDIUM_FILE = 2 };
+/* spray::SliceStatus (backend.hpp:29) */
+enum spray_slice_status { SPRAY_SLICE_OK = 0, SPRAY_SLICE_FAILED = 1, SPRAY_SLICE_TIMEOUT = 2 };
+/* spray::BatchState (engine.hpp:35) */
+enum spray_batch_state { SPRAY_BATCH_IN_FLIGHT = 0, SPRAY_BATCH_COMPLETE = 1, SPRAY_BATCH_FAILED = 2 };
+/* spray::RailHealthState (scheduler.hpp:63) */
+enum spray_health { SPRAY_HEALTHY = 0, SPRAY_EXCLUDED = 1, SPRAY_PROBING = 2 };
+/* spray::Policy (scheduler.hpp:23) */
+enum spray_policy { SPRAY_POLICY_TELEMETRY = 0, SPRAY_POLICY_RR = 1, SPRAY_POLICY_HASH = 2 };
+/* spray::FaultEffect (backend.hpp:74) */
+enum spray_fault_effect {
+  SPRAY_FAULT_DOWN = 0, SPRAY_FAULT_DEGRADE = 1, SPRAY_FAULT_JITTER = 2, SPRAY_FAULT_DROP_COMPLETION = 3
+};
+/* How a rail's bytes move on B200 (no reference analogue: the reference's rails are
+ * simulated). Chosen per rail by the topology document's "executor" key. */
+enum spray_executor {
+  SPRAY_EXEC_SM = 0,     /* SM warps, 128-bit ld/st over UVA: local HBM, NVLink peer, mapped host */
+  SPRAY_EXEC_CE = 1,     /* copy engine: cudaMemcpyAsync on a side stream, driven by a host proxy */
+  SPRAY_EXEC_RELAY = 2   /* 2-hop through an intermediate GPU's staging buffer */
+};
+
+/* ------------------------------------------------------------------ engine types */
+/* spray::BufferDesc (fabric.hpp:128-132). `data` is a device pointer for DEVICE
+ * segments and a pinned host pointer (cudaHostAlloc / cudaHostRegister) for HOST. */
+typedef struct spray_buffer_desc {
+  uint64_t offset;
+  uint64_t length;
+  void* data;
+} spray_buffer_desc;
+
+/* spray::SegmentDescriptor (fabric.hpp:134-141). */
+typedef struct spray_segment_desc {
+  const char* id;
+  int32_t medium;            /* enum spray_medium */
+  const char* node;
+  const spray_buffer_desc* buffers;
+  uint32_t n_buffers;
+  const char* device;        /* optional explicit topology device binding ("" or NULL = first of kind) */
+} spray_segment_desc;
+
+/* spray::TransferRequest (engine.hpp:73-80). */
+typedef struct spray_transfer_request {
+  const char* src_segment;
+  uint64_t src_offset;
+  const char* dst_segment;
+  uint64_t dst_offset;
+  uint64_t length;
+  int32_t direction;         /* enum spray_direction */
+} spray_transfer_request;
+
+/* spray::BatchStatus (engine.hpp:39-43). */
+typedef struct spray_batch_status {
+  int32_t state;             /* enum spray_batch_state */
+  uint64_t remaining;
+  char failure_reason[64];
+} spray_batch_status_t;
+
+/* Per-rail counters (telemetry.hpp:53-61 RailStatsView, without windows). */
+typedef struct spray_rail_stats {
+  uint64_t bytes_posted;
+  uint64_t bytes_ok;
+  uint64_t bytes_failed;
+  int64_t queue_depth;       /* scheduler queued bytes A_d */
+  double beta0, beta1;       /* cost-model state (scheduler.hpp:158-168) */
+  int32_t health;            /* enum spray_health */
+  uint32_t latency_hist[48]; /* LatencyHistogram buckets (telemetry.hpp:23-35) */
+} spray_rail_stats;
+
+typedef struct spray_engine spray_engine;
+
+/* Engine(EngineOptions) (engine.cpp:71-112). `config_json` is the documented engine
+ * config document (README "Engine config document"; unknown keys rejected,
+ * engine.cpp:1186-1197) and may be NULL for defaults; `topology_json` is the
+ * topology document (fabric.cpp:157-210) extended with per-rail "executor",
+ * "gpu" and "via" keys. `device` is the CUDA ordinal this engine drives. */
+int spray_engine_create(const char* config_json, const char* topology_json, int device,
+                        spray_engine** out);
+void spray_engine_destroy(spray_engine* e);
+int spray_engine_start(spray_engine* e);    /* Engine::start (engine.cpp:142-154) */
+int spray_engine_stop(spray_engine* e);     /* Engine::stop  (engine.cpp:156-163) */
+
+/* Engine::register_segment (engine.cpp:222-224 -> fabric.cpp:261-304). */
+int spray_register_segment(spray_engine* e, const spray_segment_desc* desc);
+
+/* Engine::allocate_batch / submit_transfer / batch_status / free_batch / await_batch
+ * (engine.cpp:228-332, 1141-1158). submit returns before any data moves. */
+int spray_allocate_batch(spray_engine* e, uint64_t* batch_out);
+int spray_submit_transfer(spray_engine* e, uint64_t batch, const spray_transfer_request* req,
+                          uint64_t* transfer_id_out);
+/* Vectorised submit: n calls of submit_transfer in order, one lock acquisition and
+ * one publication to the device submission ring. Stops at the first failing
+ * request; *n_done says how many were accepted. */
+int spray_submit_transfers(spray_engine* e, uint64_t batch, const spray_transfer_request* reqs,
+                           size_t n, uint64_t* transfer_ids_out, size_t* n_done);
+int spray_batch_status(spray_engine* e, uint64_t batch, spray_batch_status_t* out);
+int spray_await_batch(spray_engine* e, uint64_t batch, uint64_t limit_ns, spray_batch_status_t* out);
+int spray_free_batch(spray_engine* e, uint64_t batch);
+
+/* Introspection. */
+int spray_rail_count(spray_engine* e, uint32_t* n);
+int spray_rail_id(spray_engine* e, uint32_t rail, char* buf, size_t cap);
+int spray_rail_stats_get(spray_engine* e, uint32_t rail, spray_rail_stats* out);
+/* bytes_dispatched / bytes_terminated (engine.hpp:127-128): equal at quiescence. */
+int spray_engine_counters(spray_engine* e, uint64_t* bytes_dispatched, uint64_t* bytes_terminated,
+                          uint64_t* batches_failed);
+
+/* FaultSchedule entry (backend.hpp:74-94) applied to the live device fabric.
+ * Times are engine-relative nanoseconds (spray_engine_now_ns). A DOWN fault aborts
+ * in-flight slices with a partial prefix write and fails new ones
+ * (sim_backend.cpp:188-200 semantics). */
+int spray_inject_fault(spray_engine* e, const char* rail_id, int32_t effect, uint64_t start_ns,
+                       uint64_t end_ns, double factor);
+int spray_clear_faults(spray_engine* e);
+uint64_t spray_engine_now_ns(spray_engine* e);
+
+/* Heal timing of the most recent DOWN fault: fault start -> first retried slice OK,
+ * in device-clock nanoseconds (0 when not observed). */
+int spray_heal_stats(spray_engine* e, uint64_t* fault_start_ns, uint64_t* first_reroute_ok_ns,
+                     uint64_t* failed_attempts, uint64_t* retried_ok);
+
+/* ------------------------------------------------------------------ trace / replay */
+/* One scheduler-state event. A live engine records, in the exact order its device
+ * scheduler applied them, every event that changes cost-model or health state; the
+ * same stream replayed through the reference SliceScheduler/ResilienceManager (or the
+ * oracle) must reproduce every decision bit for bit. Semantics per kind:
+ *   DECIDE(set=rail, len, offset)       choose_rail(len, offset, candidate set)       (scheduler.cpp:138-195)
+ *   COMPLETE(local=rail, remote, len, status, t_ns, flags, predicted, x_norm, now=aux)
+ *        release(local,len); observe(local, remote, status, to_seconds(t_ns),
+ *        flags&MODEL ? predicted : 0, now); if status==OK && flags&MODEL && !(flags&CANCELLED)
+ *        && x_norm>0: feedback(local, to_seconds(t_ns), x_norm)          (engine.cpp:792-851)
+ *   CHARGE(rail, len) / RELEASE(rail, len)                                (scheduler.cpp:197-206)
+ *   HEALTH(rail, state=flags)          set_health                          (scheduler.hpp:136-138)
+ *   RESET(now=t_ns)                    periodic_reset(now)                 (scheduler.cpp:232-240)
+ *   RESET_RAIL(rail, now=t_ns)         reset_rail                          (scheduler.cpp:242-247)
+ *   EXPECT_HEALTH(rail, state=flags)   assertion: health(rail) == state
+ */
+enum spray_trace_kind {
+  SPRAY_EV_DECIDE = 1, SPRAY_EV_COMPLETE = 2, SPRAY_EV_CHARGE = 3, SPRAY_EV_RELEASE = 4,
+  SPRAY_EV_HEALTH = 5, SPRAY_EV_RESET = 6, SPRAY_EV_RESET_RAIL = 7, SPRAY_EV_EXPECT_HEALTH = 8
+};
+#define SPRAY_EVF_MODEL 0x1u
+#define SPRAY_EVF_CANCELLED 0x2u
+
+typedef struct spray_trace_event {  /* 64 bytes */
+  uint32_t kind;
+  uint32_t rail;      /* DECIDE: candidate-set index; else the (local) rail */
+  uint32_t remote;    /* COMPLETE: remote rail (0xffffffff = none) */
+  uint32_t flags;     /* COMPLETE: SPRAY_EVF_* | status << 8; HEALTH/EXPECT_HEALTH: the state */
+  uint64_t len;
+  uint64_t offset;    /* DECIDE: offset fed to the hash policy */
+  uint64_t t_ns;      /* COMPLETE: observed time since the decision; RESET/RESET_RAIL: now */
+  uint64_t now_ns;    /* COMPLETE: engine clock when the completion was applied */
+  double predicted;   /* COMPLETE: t_hat at dispatch */
+  double x_norm;      /* COMPLETE: x at dispatch */
+} spray_trace_event;
+
+/* spray::DispatchChoice (scheduler.hpp:98-104) plus an eligibility flag. */
+typedef struct spray_decision {  /* 32 bytes */
+  uint32_t local;
+  uint32_t remote;
+  int32_t tier;
+  uint32_t ok;        /* 0 = NoEligibleDevice (choose_rail returned nullopt) */
+  double predicted_s;
+  double x_norm;
+} spray_decision;
+
+/* Scheduler constants (spray::SchedulerConfig, scheduler.hpp:44-60). A tier penalty
+ * <= 0 encodes the reference's disengaged optional (tier unschedulable). */
+typedef struct spray_sched_config {
+  uint64_t min_slice_size;
+  uint32_t max_slices_per_transfer;
+  int32_t policy;            /* enum spray_policy */
+  double tolerance;
+  double penalty[3];         /* tiers 1..3 */
+  double ewma_alpha;
+  uint64_t reset_interval_ns;
+  double beta0_init_s;
+  double beta1_init;
+  double feedback_clamp;
+} spray_sched_config;
+
+/* Resilience constants (spray::ResilienceConfig, resilience.hpp:17-31). */
+typedef struct spray_resilience_config {
+  int32_t failure_threshold;
+  int32_t degradation_events;
+  double degradation_ratio;
+  double degradation_min_t_obs_s;
+  int32_t probe_successes_needed;
+  int32_t probe_backoff_cap;
+  uint64_t probe_bytes;
+  uint64_t probe_interval_ns;
+  double probe_backoff_mult;
+  uint32_t max_attempts;
+  uint32_t pad_;
+  uint64_t slice_timeout_ns;
+} spray_resilience_config;
+
+void spray_sched_config_default(spray_sched_config* c);
+void spray_resilience_config_default(spray_resilience_config* c);
+
+/* Candidate sets are flattened int32 streams:
+ *   [n_sets, { n_locals, { local, n_pairs, { remote, tier, affinity }* }* }*]
+ * in exactly the order orient_candidates produces (orchestrator.cpp:39-81). */
+
+/* Runs the DEVICE decision function (the same code the live engine's scheduler warp
+ * executes) over `events`, on GPU `device`. Rails are described by bandwidth, base
+ * tier and the rank of their id string in sorted order (map_remote's id tie-break,
+ * scheduler.cpp:124-136). decisions_out gets one entry per DECIDE event;
+ * *expect_failures counts EXPECT_HEALTH mismatches. */
+int spray_replay_device(int device, const spray_sched_config* sc, const spray_resilience_config* rc,
+                        uint32_t n_rails, const double* bandwidth, const int32_t* base_tier,
+                        const uint32_t* id_rank, const int32_t* cand_stream, size_t cand_len,
+                        const spray_trace_event* events, size_t n_events,
+                        spray_decision* decisions_out, size_t decisions_cap, size_t* n_decisions,
+                        uint64_t* expect_failures);
+
+/* Recorded live trace of an engine (events in application order + the decisions the
+ * device made for each DECIDE), and the candidate sets those events index. */
+int spray_trace_enable(spray_engine* e, size_t capacity_events);
+int spray_trace_fetch(spray_engine* e, spray_trace_event* events, size_t cap, size_t* n_events,
+                      spray_decision* decisions, size_t dcap, size_t* n_decisions);
+int spray_trace_candidates(spray_engine* e, int32_t* stream, size_t cap, size_t* len);
+
+/* ------------------------------------------------------------------ backend (plugin) */
+/* spray::SliceWorkRequest (backend.hpp:15-27) as a 64-byte POD: segment ids become
+ * their Hash128 (common.hpp:111-120), as on the reference TCP wire. */
+typedef struct spray_slice_wr {  /* 96 bytes */
+  uint64_t slice;
+  uint64_t batch;
+  uint64_t src_seg_lo, src_seg_hi;
+  uint64_t src_offset;
+  uint64_t dst_seg_lo, dst_seg_hi;
+  uint64_t dst_offset;   /* absolute; re-execution is byte-idempotent (backend.hpp:21) */
+  uint64_t length;
+  int32_t direction;     /* enum spray_direction */
+  uint32_t local_rail;
+  uint32_t remote_rail;
+  uint32_t attempt;
+} spray_slice_wr;
+
+/* spray::CompletionEvent (backend.hpp:33-40). */
+typedef struct spray_cqe {  /* 40 bytes */
+  uint64_t slice;
+  uint64_t batch;
+  int32_t status;     /* enum spray_slice_status */
+  uint32_t rail;
+  uint64_t t_obs_ns;
+  uint64_t bytes;
+} spray_cqe;
+
+/* spray::BackendCapabilities (fabric.hpp:207-221). */
+typedef struct spray_backend_caps {
+  char id[32];
+  uint32_t media_pairs_mask;  /* bit (src*3+dst) set when (src,dst) medium pair is covered */
+  uint8_t supports_read, supports_write, cross_node, same_node;
+  uint64_t max_post_size;
+  uint8_t batched_posting;
+  uint8_t pad_[7];
+} spray_backend_caps;
+
+typedef struct spray_backend spray_backend;
+
+int spray_backend_open(int device, spray_backend** out);
+void spray_backend_close(spray_backend* b);
+int spray_backend_start(spray_backend* b);                 /* TransportBackend::start */
+int spray_backend_stop(spray_backend* b);                  /* TransportBackend::stop  */
+int spray_backend_capabilities(spray_backend* b, spray_backend_caps* out);
+/* attach_segment_metadata (backend.hpp:65-68): registers (id hash -> buffers). Returns
+ * SPRAY_OK and writes a metadata blob, or SPRAY_ECAPABILITY when the medium is not served. */
+int spray_backend_attach_segment(spray_backend* b, const spray_segment_desc* desc,
+                                 uint8_t* blob_out, size_t blob_cap, size_t* blob_len);
+/* post_slices (backend.hpp:55-58): accepted = prefix count; a rejected suffix is
+ * backpressure. Returns SPRAY_EFATAL with *accepted = 0 once latched fatal. */
+int spray_backend_post(spray_backend* b, const spray_slice_wr* reqs, size_t n, size_t* accepted);
+/* poll_completions (backend.hpp:60-61): never blocks; single consumer. */
+int spray_backend_poll(spray_backend* b, spray_cqe* out, size_t max, size_t* n);
+int spray_backend_fatal(spray_backend* b);                 /* 1 when latched */
+int spray_backend_latch_fatal(spray_backend* b);           /* MemoryBackend::latch_fatal analogue */
+
+/* ------------------------------------------------------------------ utilities */
+/* Device-side splitmix64 fill matching the reference payload generator
+ * (common.hpp:81-97 driven as in bench.cpp:59-67): byte i of the stream is byte
+ * (i mod 8) of the (i/8)-th next_u64() of Rng(seed), tail bytes take the low byte of
+ * one further draw each. Works on device or mapped-host pointers. */
+int spray_fill_splitmix(int device, void* ptr, uint64_t n, uint64_t seed);
+/* 64-bit order-sensitive checksum (FNV-1a over 8-byte words, tail bytewise) computed
+ * on the GPU; identical to the oracle's so_checksum. */
+int spray_checksum(int device, const void* ptr, uint64_t n, uint64_t* out);
+/* Pinned, device-mapped host allocation (cudaHostAlloc Portable|Mapped). */
+int spray_host_alloc(uint64_t n, void** out);
+int spray_host_free(void* p);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SPRAY_B200_H */
