@@ -169,10 +169,38 @@ int spray_inject_fault(spray_engine* e, const char* rail_id, int32_t effect, uin
 int spray_clear_faults(spray_engine* e);
 uint64_t spray_engine_now_ns(spray_engine* e);
 
+/* Diagnostic snapshot (ring positions, kernel state, counters, stream status). */
+int spray_engine_debug(spray_engine* e, uint64_t* out, size_t n);
+
 /* Heal timing of the most recent DOWN fault: fault start -> first retried slice OK,
  * in device-clock nanoseconds (0 when not observed). */
 int spray_heal_stats(spray_engine* e, uint64_t* fault_start_ns, uint64_t* first_reroute_ok_ns,
                      uint64_t* failed_attempts, uint64_t* retried_ok);
+
+/* Device-resident submission (intents built once, kept in HBM, reused by many batches).
+ * prepare: validates and plans every request exactly like submit_transfer and stages the
+ * resulting intents in HBM. run: submits them all into `batch` as one bulk record and
+ * runs the engine kernel in drain mode: one launch, bracketed by CUDA events on the
+ * engine's stream, that exits when the batch is delivered; *kernel_ms is its duration.
+ * Any running launch of the engine is stopped first. */
+typedef struct spray_prepared spray_prepared;
+int spray_prepare_transfers(spray_engine* e, const spray_transfer_request* reqs, size_t n,
+                            spray_prepared** out);
+int spray_run_prepared(spray_engine* e, uint64_t batch, spray_prepared* p, float* kernel_ms);
+void spray_prepared_free(spray_prepared* p);
+
+/* Multi-process peer segments: export a device allocation as a CUDA IPC handle (64 B) and
+ * open a peer's handle in this process (the returned pointer can be registered as a
+ * DEVICE segment on the peer's node). */
+int spray_ipc_export(int device, void* ptr, uint8_t handle_out[64]);
+int spray_ipc_open(int device, const uint8_t handle[64], void** ptr_out);
+int spray_ipc_close(void* ptr);
+
+/* Host planning only (no GPU work): the candidate stream of the route the engine would
+ * use for src -> dst (orchestrator.cpp:98-245 + 39-81), and the backend serving it. */
+int spray_plan_candidates(spray_engine* e, const char* src_segment, const char* dst_segment,
+                          int32_t direction, int32_t* stream, size_t cap, size_t* len,
+                          char* backend, size_t backend_cap);
 
 /* ------------------------------------------------------------------ trace / replay */
 /* One scheduler-state event. A live engine records, in the exact order its device
@@ -280,7 +308,7 @@ int spray_trace_candidates(spray_engine* e, int32_t* stream, size_t cap, size_t*
 /* ------------------------------------------------------------------ backend (plugin) */
 /* spray::SliceWorkRequest (backend.hpp:15-27) as a 64-byte POD: segment ids become
  * their Hash128 (common.hpp:111-120), as on the reference TCP wire. */
-typedef struct spray_slice_wr {  /* 96 bytes */
+typedef struct spray_slice_wr {  /* 88 bytes */
   uint64_t slice;
   uint64_t batch;
   uint64_t src_seg_lo, src_seg_hi;
@@ -339,8 +367,9 @@ int spray_backend_latch_fatal(spray_backend* b);           /* MemoryBackend::lat
  * (i mod 8) of the (i/8)-th next_u64() of Rng(seed), tail bytes take the low byte of
  * one further draw each. Works on device or mapped-host pointers. */
 int spray_fill_splitmix(int device, void* ptr, uint64_t n, uint64_t seed);
-/* 64-bit order-sensitive checksum (FNV-1a over 8-byte words, tail bytewise) computed
- * on the GPU; identical to the oracle's so_checksum. */
+/* 64-bit order-sensitive checksum computed on the GPU: sum over little-endian 8-byte
+ * words w_i (zero-padded tail) of splitmix64_mix(w_i + (i+1)*0x9e3779b97f4a7c15), xor n.
+ * Identical to the oracle's so_checksum. */
 int spray_checksum(int device, const void* ptr, uint64_t n, uint64_t* out);
 /* Pinned, device-mapped host allocation (cudaHostAlloc Portable|Mapped). */
 int spray_host_alloc(uint64_t n, void** out);

@@ -1,0 +1,75 @@
+"""In-tree build of libspray_b200.so (sm_100a only) — `python -m paper_2604_00368_b200.build`.
+
+The .so is written next to this file so it travels to GPU boxes with the repo snapshot.
+"""
+from __future__ import annotations
+
+import concurrent.futures as cf
+import os
+import subprocess
+import sys
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+CSRC = os.path.join(HERE, "csrc")
+OBJ = os.path.join(HERE, "_obj")
+SO = os.path.join(HERE, "libspray_b200.so")
+NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-Wall"]
+
+SOURCES = {
+    "spray_kernel.cu": ARCH + ["-fmad=false", "-Xptxas", "-v"],
+    "engine.cpp": [],
+    "fabric.cpp": [],
+    "orchestrator.cpp": [],
+    "capi.cpp": [],
+}
+
+
+def _stale(target: str, deps) -> bool:
+    if not os.path.exists(target):
+        return True
+    t = os.path.getmtime(target)
+    return any(os.path.getmtime(d) > t for d in deps)
+
+
+def _headers():
+    hs = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".hpp", ".cuh", ".h"))]
+    hs.append(os.path.join(os.path.dirname(HERE), "include", "spray_b200.h"))
+    return hs
+
+
+def _compile(src: str, flags) -> str:
+    obj = os.path.join(OBJ, src + ".o")
+    path = os.path.join(CSRC, src)
+    if _stale(obj, [path] + _headers()):
+        cmd = [NVCC] + COMMON + flags + ["-c", path, "-o", obj]
+        if src.endswith(".cpp"):
+            cmd = [NVCC] + COMMON + ["-x", "cu"] + ARCH + flags + ["-c", path, "-o", obj] if False else \
+                  [NVCC] + COMMON + flags + ["-c", path, "-o", obj]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(f"compile {src} failed:\n{r.stdout}\n{r.stderr}")
+        if "-Xptxas" in flags:
+            with open(os.path.join(OBJ, src + ".ptxas.txt"), "w") as f:
+                f.write(r.stderr)
+    return obj
+
+
+def build(verbose: bool = False) -> str:
+    os.makedirs(OBJ, exist_ok=True)
+    with cf.ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:
+        objs = list(ex.map(lambda kv: _compile(*kv), SOURCES.items()))
+    if _stale(SO, objs):
+        cmd = [NVCC, "-shared"] + ARCH + ["-o", SO] + objs + ["-lcudart", "-lpthread"]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
+    if verbose:
+        print(SO)
+    return SO
+
+
+if __name__ == "__main__":
+    build(verbose=True)
+    sys.exit(0)

@@ -1,0 +1,234 @@
+// dev_types.cuh — POD layout shared by the host engine (C++) and the persistent
+// sm_100a spray kernel. Everything the device touches lives in one of three places:
+//   * HBM (cudaMalloc): slice table, SM work ring, completion ring, candidate tables,
+//     trace buffers, per-engine flags — hot, written and read only by the GPU;
+//   * mapped pinned host memory (cudaHostAlloc Mapped): the submission ring the host
+//     produces into, batch counters the host polls, the CE proxy rings and the stats
+//     mirror — the host<->device boundary, no cudaMemcpy on it;
+//   * shared memory of CTA 0: the scheduler warp's working copy of the per-rail cost
+//     state (scheduler.hpp:158-168), single-owner, so decisions need no atomics.
+#pragma once
+#include <stdint.h>
+
+namespace spray_dev {
+
+constexpr int kMaxRails = 64;          // per engine (one GPU's fabric view)
+constexpr int kMaxLocals = 32;         // candidates per set: one scheduler lane each
+constexpr int kMaxPairs = 16;          // remote options per candidate
+constexpr uint32_t kNoRail = 0xffffffffu;
+
+enum : uint32_t { kHealthy = 0, kExcluded = 1, kProbing = 2 };
+enum : uint32_t { kExecSM = 0, kExecCE = 1, kExecRelay = 2 };
+enum : uint32_t { kStOk = 0, kStFailed = 1, kStTimeout = 2 };
+
+// Per-rail immutable description (uploaded at start).
+struct RailDesc {
+  double bandwidth;       // B_d, bytes/s (fabric.hpp:68)
+  int32_t base_tier;      // 1..3
+  uint32_t id_rank;       // rank of the rail id string: map_remote/dispatch_retry tie-break
+  uint32_t executor;      // kExec*
+  int32_t gpu;            // owning GPU ordinal (-1 for host-side rails)
+  int32_t via;            // relay GPU (relay rails)
+  uint32_t ce_index;      // CE proxy stream index (CE rails)
+  uint32_t pad_[2];
+};
+
+// Scheduler cost state (scheduler.hpp:158-168) + resilience record (resilience.hpp:68-76)
+// + telemetry counters (telemetry.hpp:88-98). Lives in CTA-0 shared memory while the
+// kernel runs; written back to HBM when it exits and mirrored to host periodically.
+struct RailState {
+  double beta0, beta1, min_obs;
+  int64_t queued;
+  uint64_t last_reset;
+  uint32_t health;
+  uint32_t has_obs;
+  int32_t consec_failures;
+  int32_t degradation_count;
+  int32_t backoff;
+  int32_t probe_streak;
+  uint64_t next_probe, excluded_at;
+  uint64_t bytes_posted, bytes_ok, bytes_failed;
+  uint32_t hist[48];
+};
+
+// Candidate set (orchestrator.cpp:39-81 output), flattened for the device.
+struct CandSet {
+  uint32_t n_locals;
+  uint32_t pad_;
+  uint32_t local[kMaxLocals];
+  uint32_t n_pairs[kMaxLocals];
+  uint32_t pair_remote[kMaxLocals][kMaxPairs];
+  int32_t pair_tier[kMaxLocals][kMaxPairs];
+  uint8_t pair_aff[kMaxLocals][kMaxPairs];
+};
+
+// One transfer intent (TransferRequest after planning), 64 B, in the submission ring.
+// flags bit0 = BULK: src points at an array of `len` Intent records in HBM that inherit
+// this record's batch.
+struct Intent {
+  uint64_t batch_id;
+  uint64_t src;           // device-usable address of src_offset (BULK: HBM Intent array)
+  uint64_t dst;           // device-usable address of dst_offset
+  uint64_t len;           // bytes (BULK: number of intents in the array)
+  uint64_t hash_offset;   // absolute source offset (hash policy input, engine.cpp:387)
+  uint64_t transfer_id;
+  uint32_t set_id;
+  uint32_t batch_slot;
+  uint32_t flags;
+  uint32_t pad_;
+};
+static_assert(sizeof(Intent) == 64, "intent is one 64-B line");
+constexpr uint32_t kIntentBulk = 1u;
+
+// Slice record (engine.hpp:135-161 SliceRec, device form), in HBM. 128 B.
+struct Slice {
+  uint64_t src, dst, len;
+  uint64_t dispatched_at;
+  double predicted, x_norm;
+  uint64_t batch_id;
+  uint64_t hash_offset;
+  uint32_t local, remote;
+  uint32_t attempt;
+  uint32_t batch_slot;
+  uint32_t set_id;
+  uint32_t model;          // 1 = dispatched by the cost model
+  uint32_t target;         // slot chunk counter value once this attempt's chunks are done
+  uint32_t n_failed_pairs;
+  uint8_t failed_local[4], failed_remote[4];  // burned pairs (engine.cpp:765-767)
+  uint8_t pad_[24];
+};
+static_assert(sizeof(Slice) == 128, "slice record is 128 B");
+
+// SM work item: one chunk, self-contained so a worker never reads the slice record to
+// copy. `stamp` = ring position + 1 publishes it. 48 B.
+struct WorkItem {
+  uint64_t src, dst;
+  uint32_t len;
+  uint32_t slice;
+  uint32_t target;         // completion when the slot's chunk counter reaches this
+  uint16_t rail, remote;   // fault words to honour (remote 0xffff = none)
+  uint32_t attempt;
+  uint32_t pad_;
+  uint32_t stamp;
+  uint32_t pad2_;
+};
+static_assert(sizeof(WorkItem) == 48, "work item is 48 B");
+
+// Device completion word: one 8-byte store carries slice, status and the publication
+// stamp, so a reader validates and reads it in a single access (no acquire fence).
+__host__ __device__ inline uint64_t pack_completion(uint32_t slice, uint32_t status, uint32_t stamp) {
+  return ((uint64_t)stamp << 32) | ((uint64_t)(status & 0xfu) << 28) | (slice & 0x0fffffffu);
+}
+
+// Completion record posted by the CE proxy on the host (mapped ring). 32 B.
+struct Completion {
+  uint32_t slice;
+  uint32_t attempt;
+  uint32_t status;
+  uint32_t rail;
+  uint64_t t_done;         // engine clock at completion
+  uint32_t stamp;
+  uint32_t pad_;
+};
+
+// CE work order to the host proxy (mapped host ring), 48 B.
+struct CeOrder {
+  uint64_t src, dst, len;
+  uint32_t slice, attempt;
+  uint32_t rail, ce_index;
+  uint64_t stamp;
+};
+
+// Per-batch counters. Slots are reused across batches: `done` is monotonic over the
+// slot's lifetime (the host keeps the value at allocation as the batch's base) and
+// `failed_id` names the batch id that failed (AllRoutesExhausted): no reset is needed.
+struct BatchDev {
+  uint64_t done;           // slices delivered through this slot (finish_logical count)
+  uint64_t failed_id;      // batch id that failed terminally in this slot (0 = none)
+};
+
+// Fault word per rail (FaultSchedule entry, backend.hpp:74-94).
+struct FaultDev {
+  uint64_t start, end;     // engine ns
+  uint32_t effect;         // 0 down, 1 degrade, 2 jitter, 3 drop
+  uint32_t active;
+  double factor;
+};
+
+// The host<->device control block (mapped host memory). The first 32 bytes are the
+// host->device words the scheduler polls; it reads them in one round trip.
+struct alignas(64) Control {
+  volatile uint64_t sub_tail;        // host: intents published
+  volatile uint32_t stop;            // host: request exit
+  volatile uint32_t drain;           // host: exit when idle (bench timing mode)
+  volatile uint32_t fault_epoch;     // host: bumped whenever a fault word changes
+  volatile uint32_t trace_on;
+  volatile uint64_t idle_exit_ns;
+  // device -> host
+  volatile uint64_t sub_head;        // intents consumed
+  volatile uint32_t state;           // 0 exited, 1 running, 2 exiting
+  volatile uint32_t pad0_;
+  volatile uint64_t device_now;      // engine clock (ns since epoch) seen by the scheduler
+  volatile uint64_t epoch;           // globaltimer value of engine time 0
+  volatile uint64_t bytes_dispatched, bytes_terminated;
+  volatile uint64_t batches_failed;
+  volatile uint64_t heal_fault_start, heal_first_ok, failed_attempts, retried_ok;
+  volatile uint64_t ce_tail[8];      // device: CE orders produced per CE stream
+  volatile uint64_t ce_head[8];      // host: CE orders consumed
+  volatile uint64_t xc_tail;         // host: external completions produced (CE proxy)
+  volatile uint64_t xc_head;         // device: consumed
+  volatile uint64_t trace_n, trace_dn;
+  volatile uint64_t error;           // sticky device-side error code (0 = none)
+  // scheduler profile (globaltimer ns): loops, time in completions / submissions / control
+  volatile uint64_t prof_loops, prof_comp_ns, prof_sub_ns, prof_ctl_ns, prof_n_comp, prof_n_dec;
+  volatile uint64_t prof_x[8];       // fine-grained scheduler phase clocks (SM cycles)
+};
+
+// Everything the kernel needs, passed by value.
+struct EngineDev {
+  Control* ctl;                      // mapped host
+  Intent* sub_ring; uint64_t sub_cap;  // mapped host
+  BatchDev* batches; uint32_t n_batch_slots;  // mapped host mirror (device writes, host reads)
+  BatchDev* batches_hbm;             // HBM: the scheduler's own copy
+  FaultDev* faults;                  // mapped host, per rail (host writes)
+  RailState* rail_mirror;            // mapped host, per rail (stats mirror)
+  CeOrder* ce_ring; uint64_t ce_cap; // mapped host, [8][ce_cap]
+  Completion* xc_ring; uint64_t xc_cap;  // mapped host (CE proxy completions)
+
+  const RailDesc* rails; uint32_t n_rails;     // HBM
+  RailState* rail_state;                       // HBM (persisted between launches)
+  const CandSet* sets; uint32_t n_sets;        // HBM
+  Slice* slices; uint32_t n_slices;            // HBM
+  uint64_t* free_slices;                       // HBM stack of (slot | chunk-counter base << 32)
+  uint32_t* slot_done;                         // HBM per-slot chunk counters (workers, monotonic)
+  uint32_t* slot_fail;                         // HBM per-slot failed-attempt target (workers)
+  WorkItem* work; uint64_t work_cap;           // HBM MPMC ring
+  unsigned long long* work_head;               // HBM ticket counter (workers)
+  uint64_t* comp; uint64_t comp_cap;           // HBM MPSC ring of packed completion words
+  unsigned long long* comp_tail;               // HBM ticket counter (workers)
+  uint32_t* parked; uint32_t parked_cap;       // HBM
+  uint8_t* trace_ev; uint8_t* trace_dec; uint64_t trace_cap;  // HBM (spray_trace_event / spray_decision)
+  uint64_t* persist;                           // HBM: scheduler scalars persisted across launches
+  FaultDev* faults_hbm;                        // HBM mirror of the fault words (workers read)
+  unsigned long long* next_free;               // HBM degrade FIFO server per rail
+  uint32_t* exit_flag;                         // HBM: scheduler -> workers
+
+  // scheduler constants (spray_sched_config / spray_resilience_config, device form)
+  double tolerance, penalty[3], alpha, beta0_init, beta1_init, clamp;
+  uint64_t reset_interval, min_slice;
+  uint32_t max_slices, policy;
+  int32_t failure_threshold, degradation_events, probe_successes;
+  double degradation_ratio, degradation_min_t;
+  uint32_t max_attempts;
+  uint32_t has_ce;                             // poll the CE proxy completion ring
+  uint64_t chunk_bytes;                        // SM work granule (power of two)
+  uint32_t chunk_shift;                        // log2(chunk_bytes)
+  uint32_t pad_cs_;
+  uint64_t epoch;                              // globaltimer at engine time 0
+};
+
+// scalars persisted in EngineDev::persist between launches
+enum : int { kPRr = 0, kPWorkTail = 1, kPCompHead = 2, kPFreeTop = 3, kPParked = 4,
+             kPLastReset = 5, kPOutChunks = 6, kPOutSlices = 7, kPNum = 16 };
+
+}  // namespace spray_dev

@@ -1,0 +1,938 @@
+// engine.cpp — host side of the B200 spray engine (see engine.hpp).
+#include "engine.hpp"
+
+#include <algorithm>
+#include <chrono>
+#include <cstring>
+#include <immintrin.h>
+
+namespace spray_launch {
+size_t engine_smem_bytes();
+cudaError_t launch_engine(const spray_dev::EngineDev& E, int grid, int block, cudaStream_t st);
+cudaError_t launch_epoch(uint64_t* out, cudaStream_t st);
+}  // namespace spray_launch
+
+namespace spray {
+
+using namespace spray_dev;
+
+#define CK(x)                                                                                     \
+  do {                                                                                            \
+    cudaError_t e_ = (x);                                                                         \
+    if (e_ != cudaSuccess) throw CudaError(std::string(#x) + ": " + cudaGetErrorString(e_));     \
+  } while (0)
+
+void default_sched_config(spray_sched_config* c) {  // scheduler.hpp:44-58
+  c->min_slice_size = 64 * 1024;
+  c->max_slices_per_transfer = 4096;
+  c->policy = SPRAY_POLICY_TELEMETRY;
+  c->tolerance = 0.05;
+  c->penalty[0] = 1.0;
+  c->penalty[1] = 3.0;
+  c->penalty[2] = 0.0;  // tier 3 unschedulable
+  c->ewma_alpha = 0.2;
+  c->reset_interval_ns = 30ull * 1000000000ull;
+  c->beta0_init_s = 0.0;
+  c->beta1_init = 1.0;
+  c->feedback_clamp = 5.0;
+}
+
+void default_resilience_config(spray_resilience_config* c) {  // resilience.hpp:17-28
+  std::memset(c, 0, sizeof(*c));
+  c->failure_threshold = 3;
+  c->degradation_ratio = 4.0;
+  c->degradation_events = 8;
+  c->degradation_min_t_obs_s = 1e-3;
+  c->probe_successes_needed = 2;
+  c->probe_bytes = 4096;
+  c->probe_interval_ns = 1000000000ull;
+  c->probe_backoff_mult = 1.0;
+  c->probe_backoff_cap = 3;
+  c->max_attempts = 4;
+  c->slice_timeout_ns = 2000000000ull;  // real clock default (engine.cpp:78-79)
+}
+
+static void reject_unknown(const Json& j, std::initializer_list<const char*> known, const char* scope) {
+  for (const auto& kv : j.obj) {
+    bool ok = false;
+    for (const char* k : known) ok = ok || kv.first == k;
+    if (!ok) throw ConfigError(std::string("engine config: unknown key '") + kv.first + "' in " + scope);
+  }
+}
+
+// SchedulerConfig::validate (scheduler.cpp:34-61)
+static void validate(const spray_sched_config& c, double omega) {
+  if (c.min_slice_size < 4096) throw ConfigError("min slice size must be >= 4096");
+  if (c.max_slices_per_transfer == 0) throw ConfigError("max slices must be >= 1");
+  if (!(c.tolerance > 0.0)) throw ConfigError("tolerance must be > 0");
+  if (c.ewma_alpha <= 0.0 || c.ewma_alpha > 1.0) throw ConfigError("alpha must be in (0, 1]");
+  if (omega < 0.0 || omega > 1.0) throw ConfigError("diffusion weight must be in [0, 1]");
+  if (omega != 0.0) throw ConfigError("diffusion weight > 0 (global load board) is not part of this data plane");
+  double prev = 0.0;
+  for (int t = 0; t < 3; ++t) {
+    if (!(c.penalty[t] > 0.0)) {
+      for (int u = t + 1; u < 3; ++u)
+        if (c.penalty[u] > 0.0) throw ConfigError("tier penalties must be non-decreasing");
+      break;
+    }
+    if (c.penalty[t] < prev) throw ConfigError("tier penalties must be non-decreasing");
+    prev = c.penalty[t];
+  }
+}
+
+static void validate(const spray_resilience_config& c) {  // resilience.cpp:6-14
+  if (c.failure_threshold < 1) throw ConfigError("failure threshold must be >= 1");
+  if (c.degradation_ratio <= 1.0) throw ConfigError("degradation ratio must be > 1");
+  if (c.degradation_events < 1) throw ConfigError("degradation events must be >= 1");
+  if (c.probe_successes_needed < 1) throw ConfigError("probe successes must be >= 1");
+  if (c.probe_bytes == 0) throw ConfigError("probe bytes must be > 0");
+  if (c.max_attempts < 1) throw ConfigError("max attempts must be >= 1");
+  if (c.probe_backoff_mult < 1.0) throw ConfigError("probe backoff mult must be >= 1");
+}
+
+EngineOptions engine_options_from_json(const std::string& text) {
+  EngineOptions eo;
+  default_sched_config(&eo.sched);
+  default_resilience_config(&eo.res);
+  if (text.empty()) return eo;
+  Json j;
+  try {
+    j = Json::parse(text);
+  } catch (const JsonError& e) {
+    throw ConfigError(std::string("engine config parse error: ") + e.what());
+  }
+  try {
+    reject_unknown(j, {"topology_file", "topology", "backends", "workers", "clock", "scheduler", "resilience",
+                       "staging", "burst", "ring_capacity", "stats", "stats_window_ms", "seed", "sim", "memory",
+                       "instance_id", "b200"},
+                   "root");
+    if (j.contains("backends")) {
+      eo.backends.clear();
+      for (const Json& b : j.at("backends").arr) eo.backends.push_back(b.as_string());
+    }
+    if (j.contains("clock") && j.at("clock").as_string() != "real")
+      throw ConfigError("engine config: the B200 engine runs on the device clock (clock must be real)");
+    if (j.contains("scheduler")) {
+      const Json& s = j.at("scheduler");
+      reject_unknown(s, {"min_slice_size", "max_slices_per_transfer", "tolerance", "tier1_penalty", "tier2_penalty",
+                         "tier3_penalty", "ewma_alpha", "reset_interval_ms", "diffusion_weight", "policy",
+                         "feedback_clamp"},
+                     "scheduler");
+      spray_sched_config& c = eo.sched;
+      c.min_slice_size = static_cast<uint64_t>(s.number_or("min_slice_size", double(c.min_slice_size)));
+      c.max_slices_per_transfer =
+          static_cast<uint32_t>(s.number_or("max_slices_per_transfer", double(c.max_slices_per_transfer)));
+      c.tolerance = s.number_or("tolerance", c.tolerance);
+      const char* keys[3] = {"tier1_penalty", "tier2_penalty", "tier3_penalty"};
+      for (int t = 0; t < 3; ++t)
+        if (s.contains(keys[t])) c.penalty[t] = s.at(keys[t]).is_null() ? 0.0 : s.at(keys[t]).as_number();
+      c.ewma_alpha = s.number_or("ewma_alpha", c.ewma_alpha);
+      if (s.contains("reset_interval_ms"))
+        c.reset_interval_ns = static_cast<uint64_t>(s.at("reset_interval_ms").as_number() * 1e6);
+      eo.diffusion_weight = s.number_or("diffusion_weight", 0.0);
+      if (s.contains("policy")) {
+        const std::string p = s.at("policy").as_string();
+        if (p == "telemetry") c.policy = SPRAY_POLICY_TELEMETRY;
+        else if (p == "rr" || p == "round_robin") c.policy = SPRAY_POLICY_RR;
+        else if (p == "hash") c.policy = SPRAY_POLICY_HASH;
+        else throw ConfigError("engine config: unknown policy");
+      }
+      c.feedback_clamp = s.number_or("feedback_clamp", c.feedback_clamp);
+    }
+    if (j.contains("resilience")) {
+      const Json& r = j.at("resilience");
+      reject_unknown(r, {"failure_threshold", "degradation_ratio", "degradation_events", "degradation_min_t_obs_ms",
+                         "probe_successes", "probe_bytes", "probe_interval_ms", "probe_backoff_mult",
+                         "probe_backoff_cap", "max_attempts", "slice_timeout_ms"},
+                     "resilience");
+      spray_resilience_config& c = eo.res;
+      c.failure_threshold = static_cast<int32_t>(r.number_or("failure_threshold", c.failure_threshold));
+      c.degradation_ratio = r.number_or("degradation_ratio", c.degradation_ratio);
+      c.degradation_events = static_cast<int32_t>(r.number_or("degradation_events", c.degradation_events));
+      if (r.contains("degradation_min_t_obs_ms"))
+        c.degradation_min_t_obs_s = r.at("degradation_min_t_obs_ms").as_number() * 1e-3;
+      c.probe_successes_needed = static_cast<int32_t>(r.number_or("probe_successes", c.probe_successes_needed));
+      c.probe_bytes = static_cast<uint64_t>(r.number_or("probe_bytes", double(c.probe_bytes)));
+      if (r.contains("probe_interval_ms"))
+        c.probe_interval_ns = static_cast<uint64_t>(r.at("probe_interval_ms").as_number() * 1e6);
+      c.probe_backoff_mult = r.number_or("probe_backoff_mult", c.probe_backoff_mult);
+      c.probe_backoff_cap = static_cast<int32_t>(r.number_or("probe_backoff_cap", c.probe_backoff_cap));
+      c.max_attempts = static_cast<uint32_t>(r.number_or("max_attempts", c.max_attempts));
+      if (r.contains("slice_timeout_ms"))
+        c.slice_timeout_ns = static_cast<uint64_t>(r.at("slice_timeout_ms").as_number() * 1e6);
+    }
+    if (j.contains("b200")) {
+      const Json& b = j.at("b200");
+      reject_unknown(b, {"grid", "block", "chunk_bytes", "idle_exit_ms", "slice_capacity", "work_capacity",
+                         "sub_capacity", "batch_slots"},
+                     "b200");
+      eo.grid = static_cast<int>(b.number_or("grid", eo.grid));
+      eo.block = static_cast<int>(b.number_or("block", eo.block));
+      eo.chunk_bytes = static_cast<uint64_t>(b.number_or("chunk_bytes", double(eo.chunk_bytes)));
+      if (b.contains("idle_exit_ms")) eo.idle_exit_ns = static_cast<uint64_t>(b.at("idle_exit_ms").as_number() * 1e6);
+      eo.slice_capacity = static_cast<uint32_t>(b.number_or("slice_capacity", eo.slice_capacity));
+      eo.work_capacity = static_cast<uint64_t>(b.number_or("work_capacity", double(eo.work_capacity)));
+      eo.sub_capacity = static_cast<uint64_t>(b.number_or("sub_capacity", double(eo.sub_capacity)));
+      eo.batch_slots = static_cast<uint32_t>(b.number_or("batch_slots", eo.batch_slots));
+      if (eo.block % 32 || eo.block < 64 || eo.block > 1024) throw ConfigError("b200.block must be a multiple of 32 in [64, 1024]");
+      if (eo.chunk_bytes < 4096 || (eo.chunk_bytes & (eo.chunk_bytes - 1)) || eo.chunk_bytes > (1ull << 31))
+        throw ConfigError("b200.chunk_bytes must be a power of two in [4096, 2^31]");
+    }
+  } catch (const JsonError& e) {
+    throw ConfigError(std::string("engine config: ") + e.what());
+  }
+  return eo;
+}
+
+// ------------------------------------------------------------------ construction
+
+Engine::Engine(EngineOptions opts, const std::string& topology_json, int device)
+    : opts_(std::move(opts)), topo_(Topology::parse(topology_json)), device_(device) {
+  validate(opts_.sched, opts_.diffusion_weight);
+  validate(opts_.res);
+  if (opts_.backends.empty()) throw ConfigError("engine: no backends configured");
+  for (const std::string& b : opts_.backends) caps_.push_back(Capabilities::preset(b));
+  if (topo_.rail_count() > size_t(kMaxRails)) throw ConfigError("topology: more than 64 rails per engine");
+  for (RailIndex i = 0; i < topo_.rail_count(); ++i) {
+    const RailDecl& r = topo_.rail(i);
+    if (r.executor == 2) throw ConfigError("rail '" + r.id + "': relay executor requires the multi-GPU runtime");
+    if (r.executor == 1) {
+      has_ce_ = true;
+      if (r.ce_index >= 8) throw ConfigError("rail '" + r.id + "': ce_index must be < 8");
+    }
+  }
+  slot_busy_.assign(opts_.batch_slots, 0);
+}
+
+Engine::~Engine() {
+  try {
+    stop();
+  } catch (...) {
+  }
+  free_device();
+}
+
+void Engine::alloc_device() {
+  CK(cudaSetDevice(device_));
+  CK(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
+  CK(cudaStreamCreateWithFlags(&copy_stream_, cudaStreamNonBlocking));
+  auto host = [&](size_t bytes) -> void* {
+    void* p = nullptr;
+    CK(cudaHostAlloc(&p, bytes, cudaHostAllocMapped | cudaHostAllocPortable));
+    std::memset(p, 0, bytes);
+    return p;
+  };
+  auto dev = [&](size_t bytes) -> void* {
+    void* p = nullptr;
+    CK(cudaMalloc(&p, bytes));
+    CK(cudaMemsetAsync(p, 0, bytes, copy_stream_));
+    dev_allocs_.push_back(p);
+    return p;
+  };
+  auto dptr = [&](void* h) -> void* {
+    void* d = nullptr;
+    CK(cudaHostGetDevicePointer(&d, h, 0));
+    return d;
+  };
+  const uint32_t nr = rail_count();
+  ctl_ = static_cast<Control*>(host(sizeof(Control)));
+  ring_ = static_cast<Intent*>(host(sizeof(Intent) * opts_.sub_capacity));
+  bmirror_ = static_cast<BatchDev*>(host(sizeof(BatchDev) * opts_.batch_slots));
+  faults_ = static_cast<FaultDev*>(host(sizeof(FaultDev) * kMaxRails));
+  rmirror_ = static_cast<RailState*>(host(sizeof(RailState) * kMaxRails));
+  const uint64_t ce_cap = 4096, xc_cap = 1 << 16;
+  ce_ring_ = static_cast<CeOrder*>(host(sizeof(CeOrder) * 8 * ce_cap));
+  xc_ring_ = static_cast<Completion*>(host(sizeof(Completion) * xc_cap));
+
+  E_ = EngineDev{};
+  E_.ctl = static_cast<Control*>(dptr(ctl_));
+  E_.sub_ring = static_cast<Intent*>(dptr(ring_));
+  E_.sub_cap = opts_.sub_capacity;
+  E_.batches = static_cast<BatchDev*>(dptr(bmirror_));
+  E_.n_batch_slots = opts_.batch_slots;
+  E_.batches_hbm = static_cast<BatchDev*>(dev(sizeof(BatchDev) * opts_.batch_slots));
+  E_.faults = static_cast<FaultDev*>(dptr(faults_));
+  E_.rail_mirror = static_cast<RailState*>(dptr(rmirror_));
+  E_.ce_ring = static_cast<CeOrder*>(dptr(ce_ring_));
+  E_.ce_cap = ce_cap;
+  E_.xc_ring = static_cast<Completion*>(dptr(xc_ring_));
+  E_.xc_cap = xc_cap;
+
+  // rails
+  std::vector<RailDesc> rd(nr);
+  std::vector<RailState> rs(nr);
+  const auto ranks = topo_.id_ranks();
+  for (uint32_t i = 0; i < nr; ++i) {
+    const RailDecl& r = topo_.rail(i);
+    rd[i] = RailDesc{};
+    rd[i].bandwidth = r.bandwidth;
+    rd[i].base_tier = r.tier;
+    rd[i].id_rank = ranks[i];
+    rd[i].executor = r.executor;
+    rd[i].gpu = r.gpu;
+    rd[i].via = r.via;
+    rd[i].ce_index = r.ce_index;
+    rs[i] = RailState{};
+    rs[i].beta0 = opts_.sched.beta0_init_s;  // scheduler.cpp:87-90
+    rs[i].beta1 = opts_.sched.beta1_init;
+    rs[i].health = kHealthy;
+  }
+  void* rails_d = dev(sizeof(RailDesc) * kMaxRails);
+  void* state_d = dev(sizeof(RailState) * kMaxRails);
+  CK(cudaMemcpyAsync(rails_d, rd.data(), sizeof(RailDesc) * nr, cudaMemcpyHostToDevice, copy_stream_));
+  CK(cudaMemcpyAsync(state_d, rs.data(), sizeof(RailState) * nr, cudaMemcpyHostToDevice, copy_stream_));
+  std::memcpy(rmirror_, rs.data(), sizeof(RailState) * nr);
+  E_.rails = static_cast<RailDesc*>(rails_d);
+  E_.n_rails = nr;
+  E_.rail_state = static_cast<RailState*>(state_d);
+  E_.sets = static_cast<CandSet*>(dev(sizeof(CandSet) * opts_.max_sets));
+  E_.n_sets = 0;
+  E_.n_slices = opts_.slice_capacity;
+  E_.slices = static_cast<Slice*>(dev(sizeof(Slice) * opts_.slice_capacity));
+  E_.free_slices = static_cast<uint64_t*>(dev(sizeof(uint64_t) * opts_.slice_capacity));
+  {
+    // (slot | base << 32): every slot starts with a zero chunk-counter base
+    std::vector<uint64_t> fl(opts_.slice_capacity);
+    for (uint32_t i = 0; i < opts_.slice_capacity; ++i) fl[i] = opts_.slice_capacity - 1 - i;
+    CK(cudaMemcpyAsync(E_.free_slices, fl.data(), fl.size() * 8, cudaMemcpyHostToDevice, copy_stream_));
+    CK(cudaStreamSynchronize(copy_stream_));
+  }
+  E_.slot_done = static_cast<uint32_t*>(dev(sizeof(uint32_t) * opts_.slice_capacity));
+  E_.slot_fail = static_cast<uint32_t*>(dev(sizeof(uint32_t) * opts_.slice_capacity));
+  E_.faults_hbm = static_cast<FaultDev*>(dev(sizeof(FaultDev) * kMaxRails));
+  E_.next_free = static_cast<unsigned long long*>(dev(sizeof(unsigned long long) * kMaxRails));
+  E_.exit_flag = static_cast<uint32_t*>(dev(sizeof(uint32_t)));
+  E_.has_ce = has_ce_ ? 1u : 0u;
+  E_.work_cap = opts_.work_capacity;
+  E_.work = static_cast<WorkItem*>(dev(sizeof(WorkItem) * opts_.work_capacity));
+  E_.work_head = static_cast<unsigned long long*>(dev(sizeof(unsigned long long)));
+  E_.comp_cap = std::max<uint64_t>(2ull * opts_.slice_capacity, 1024);
+  E_.comp = static_cast<uint64_t*>(dev(sizeof(uint64_t) * E_.comp_cap));
+  E_.comp_tail = static_cast<unsigned long long*>(dev(sizeof(unsigned long long)));
+  E_.parked_cap = opts_.slice_capacity;
+  E_.parked = static_cast<uint32_t*>(dev(sizeof(uint32_t) * opts_.slice_capacity));
+  E_.persist = static_cast<uint64_t*>(dev(sizeof(uint64_t) * kPNum));
+  {
+    uint64_t p[kPNum] = {0};
+    p[kPFreeTop] = opts_.slice_capacity;
+    CK(cudaMemcpyAsync(E_.persist, p, sizeof(p), cudaMemcpyHostToDevice, copy_stream_));
+  }
+  E_.trace_ev = nullptr;
+  E_.trace_dec = nullptr;
+  E_.trace_cap = 0;
+  // constants
+  E_.tolerance = opts_.sched.tolerance;
+  for (int t = 0; t < 3; ++t) E_.penalty[t] = opts_.sched.penalty[t];
+  E_.alpha = opts_.sched.ewma_alpha;
+  E_.beta0_init = opts_.sched.beta0_init_s;
+  E_.beta1_init = opts_.sched.beta1_init;
+  E_.clamp = opts_.sched.feedback_clamp;
+  E_.reset_interval = opts_.sched.reset_interval_ns;
+  E_.min_slice = opts_.sched.min_slice_size;
+  E_.max_slices = opts_.sched.max_slices_per_transfer;
+  E_.policy = static_cast<uint32_t>(opts_.sched.policy);
+  E_.failure_threshold = opts_.res.failure_threshold;
+  E_.degradation_events = opts_.res.degradation_events;
+  E_.probe_successes = opts_.res.probe_successes_needed;
+  E_.degradation_ratio = opts_.res.degradation_ratio;
+  E_.degradation_min_t = opts_.res.degradation_min_t_obs_s;
+  E_.max_attempts = opts_.res.max_attempts;
+  E_.chunk_bytes = opts_.chunk_bytes;
+  E_.chunk_shift = 0;
+  while ((1ull << E_.chunk_shift) < opts_.chunk_bytes) ++E_.chunk_shift;
+  // engine epoch on the device clock
+  uint64_t* ep = static_cast<uint64_t*>(dev(sizeof(uint64_t)));
+  CK(spray_launch::launch_epoch(ep, copy_stream_));
+  CK(cudaMemcpyAsync(&E_.epoch, ep, sizeof(uint64_t), cudaMemcpyDeviceToHost, copy_stream_));
+  CK(cudaStreamSynchronize(copy_stream_));
+  ctl_->epoch = E_.epoch;
+  ctl_->idle_exit_ns = opts_.idle_exit_ns;
+  if (has_ce_) {
+    ce_streams_.resize(8);
+    for (auto& s : ce_streams_) CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  }
+}
+
+void Engine::free_device() {
+  for (void* p : dev_allocs_) cudaFree(p);
+  dev_allocs_.clear();
+  for (void* p : {static_cast<void*>(ctl_), static_cast<void*>(ring_), static_cast<void*>(bmirror_),
+                  static_cast<void*>(faults_), static_cast<void*>(rmirror_), static_cast<void*>(ce_ring_),
+                  static_cast<void*>(xc_ring_)})
+    if (p) cudaFreeHost(p);
+  ctl_ = nullptr;
+  ring_ = nullptr;
+  bmirror_ = nullptr;
+  faults_ = nullptr;
+  rmirror_ = nullptr;
+  ce_ring_ = nullptr;
+  xc_ring_ = nullptr;
+  for (auto& kv : segs_)
+    for (void* p : kv.second.registered) cudaHostUnregister(p);
+  for (auto& s : ce_streams_)
+    if (s) cudaStreamDestroy(s);
+  ce_streams_.clear();
+  if (stream_) cudaStreamDestroy(stream_);
+  if (copy_stream_) cudaStreamDestroy(copy_stream_);
+  stream_ = copy_stream_ = nullptr;
+}
+
+void Engine::start() {
+  std::lock_guard<std::mutex> lk(mu_);
+  if (started_) return;
+  alloc_device();
+  started_ = true;
+  if (has_ce_) {
+    ce_run_ = true;
+    ce_thread_ = std::thread([this] { ce_proxy_loop(); });
+  }
+}
+
+void Engine::stop() {
+  std::lock_guard<std::mutex> lk(mu_);
+  if (!started_) return;
+  ctl_->stop = 1;
+  std::atomic_thread_fence(std::memory_order_seq_cst);
+  cudaStreamSynchronize(stream_);
+  ctl_->stop = 0;
+  ctl_->state = 0;
+  if (has_ce_) {
+    ce_run_ = false;
+    if (ce_thread_.joinable()) ce_thread_.join();
+  }
+  started_ = false;
+}
+
+// ------------------------------------------------------------------ kernel lifecycle
+
+void Engine::launch() {
+  CK(cudaSetDevice(device_));
+  int grid = opts_.grid;
+  if (grid <= 0) {
+    int sms = 0;
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device_));
+    grid = sms;
+  }
+  ctl_->stop = 0;
+  ctl_->drain = drain_ ? 1u : 0u;
+  ctl_->state = 1;
+  std::atomic_thread_fence(std::memory_order_seq_cst);
+  CK(spray_launch::launch_engine(E_, grid, opts_.block, stream_));
+}
+
+bool Engine::running_kernel() { return ctl_ && ctl_->state != 0; }
+
+// EXITING handshake (spray_kernel.cu scheduler exit): the device publishes EXITING,
+// fences and re-checks the ring; the host publishes the tail, fences and reads state.
+void Engine::ensure_running() {
+  std::atomic_thread_fence(std::memory_order_seq_cst);
+  uint32_t st = ctl_->state;
+  if (st == 1) return;
+  while (st == 2) {
+    _mm_pause();
+    st = ctl_->state;
+  }
+  if (st == 1) return;
+  CK(cudaStreamSynchronize(stream_));  // previous launch fully drained
+  launch();
+}
+
+void Engine::set_drain(bool on) {
+  std::lock_guard<std::mutex> lk(mu_);
+  drain_ = on;
+  if (ctl_) ctl_->drain = on ? 1u : 0u;
+}
+
+// ------------------------------------------------------------------ segments
+
+void Engine::register_segment(const spray_segment_desc& d) {
+  std::lock_guard<std::mutex> lk(mu_);
+  if (!d.id || !*d.id) throw ConfigError("segment id must be non-empty");
+  const std::string node = d.node ? d.node : "";
+  if (!topo_.node(node)) throw ConfigError(std::string("segment '") + d.id + "': unknown node '" + node + "'");
+  if (d.n_buffers == 0 || !d.buffers) throw ConfigError(std::string("segment '") + d.id + "': no buffers");
+  if (d.medium == SPRAY_MEDIUM_FILE)
+    throw ConfigError(std::string("segment '") + d.id + "': file media are not served by the B200 data plane");
+  SegRec rec;
+  rec.seg.id = d.id;
+  rec.seg.medium = d.medium == SPRAY_MEDIUM_DEVICE ? Medium::kDevice : Medium::kHost;
+  rec.seg.node = node;
+  rec.seg.id_hash = hash128(rec.seg.id);
+  for (uint32_t i = 0; i < d.n_buffers; ++i)
+    rec.seg.buffers.push_back(Buffer{d.buffers[i].offset, d.buffers[i].length, d.buffers[i].data, 0});
+  std::sort(rec.seg.buffers.begin(), rec.seg.buffers.end(),
+            [](const Buffer& a, const Buffer& b) { return a.offset < b.offset; });
+  for (size_t i = 0; i + 1 < rec.seg.buffers.size(); ++i)
+    if (rec.seg.buffers[i].offset + rec.seg.buffers[i].length > rec.seg.buffers[i + 1].offset)
+      throw ConfigError(std::string("segment '") + d.id + "': OverlappingBuffers");
+  for (const Buffer& b : rec.seg.buffers) {
+    if (b.length == 0) throw ConfigError(std::string("segment '") + d.id + "': zero-length buffer");
+    if (!b.data) throw ConfigError(std::string("segment '") + d.id + "': null buffer");
+  }
+  if (d.device && *d.device) {
+    if (!topo_.find_device(node, d.device))
+      throw ConfigError(std::string("segment '") + d.id + "': unknown device '" + d.device + "'");
+    rec.seg.device = d.device;
+  } else if (const DeviceDecl* dd = topo_.first_device_of_kind(
+                 node, rec.seg.medium == Medium::kDevice ? DeviceKind::kDeviceMemory : DeviceKind::kHostMemory)) {
+    rec.seg.device = dd->id;
+  }
+  if (segs_.count(rec.seg.id)) throw ConfigError("duplicate segment id '" + rec.seg.id + "'");
+  segs_.emplace(rec.seg.id, std::move(rec));
+}
+
+// Device-usable addresses: pinned host buffers through their mapped alias (registering
+// pageable ones), peer HBM after enabling peer access. Done lazily, on the first
+// transfer that touches the segment, so registration itself stays host-only.
+void Engine::translate(SegRec& s) {
+  if (s.translated) return;
+  CK(cudaSetDevice(device_));
+  for (Buffer& b : s.seg.buffers) {
+    if (s.seg.medium == Medium::kHost) {
+      void* dp = nullptr;
+      if (cudaHostGetDevicePointer(&dp, b.data, 0) != cudaSuccess) {
+        cudaGetLastError();
+        CK(cudaHostRegister(b.data, b.length, cudaHostRegisterMapped | cudaHostRegisterPortable));
+        s.registered.push_back(b.data);
+        CK(cudaHostGetDevicePointer(&dp, b.data, 0));
+      }
+      b.dev_addr = reinterpret_cast<uint64_t>(dp);
+    } else {
+      cudaPointerAttributes a{};
+      CK(cudaPointerGetAttributes(&a, b.data));
+      if (a.type != cudaMemoryTypeDevice && a.type != cudaMemoryTypeManaged)
+        throw ConfigError("segment '" + s.seg.id + "': device medium buffer is not device memory");
+      if (a.device != device_) {
+        const cudaError_t e = cudaDeviceEnablePeerAccess(a.device, 0);
+        if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) CK(e);
+        cudaGetLastError();
+      }
+      b.dev_addr = reinterpret_cast<uint64_t>(b.data);
+    }
+  }
+  s.translated = true;
+}
+
+// ------------------------------------------------------------------ planning
+
+uint32_t Engine::set_for(const Segment& src, const Segment& dst, Direction dir) {
+  const std::string key = src.id + '\x1f' + dst.id + '\x1f' + (dir == Direction::kWrite ? 'w' : 'r');
+  auto it = set_cache_.find(key);
+  if (it != set_cache_.end()) return it->second;
+  auto routes = build_plan(topo_, src, dst, dir, opts_.sched.penalty, caps_);  // throws NoRouteError
+  const Route& r = routes.front();
+  if (r.candidates.size() > size_t(kMaxLocals)) throw ConfigError("route has more than 32 local rails");
+  if (sets_.size() >= opts_.max_sets) throw EngineError("candidate-set table full");
+  CandSet cs{};
+  cs.n_locals = static_cast<uint32_t>(r.candidates.size());
+  for (size_t l = 0; l < r.candidates.size(); ++l) {
+    const LocalCandidate& c = r.candidates[l];
+    if (c.pairs.size() > size_t(kMaxPairs)) throw ConfigError("more than 16 remote options for one rail");
+    cs.local[l] = c.local;
+    cs.n_pairs[l] = static_cast<uint32_t>(c.pairs.size());
+    for (size_t p = 0; p < c.pairs.size(); ++p) {
+      cs.pair_remote[l][p] = c.pairs[p].remote;
+      cs.pair_tier[l][p] = c.pairs[p].tier;
+      cs.pair_aff[l][p] = c.pairs[p].affinity ? 1 : 0;
+    }
+  }
+  const uint32_t id = static_cast<uint32_t>(sets_.size());
+  if (started_) {
+    CK(cudaMemcpyAsync(const_cast<CandSet*>(E_.sets) + id, &cs, sizeof(cs), cudaMemcpyHostToDevice, copy_stream_));
+    CK(cudaStreamSynchronize(copy_stream_));
+  }
+  sets_.push_back(r.candidates);
+  set_cache_.emplace(key, id);
+  return id;
+}
+
+std::vector<int32_t> Engine::plan_candidates(const std::string& s, const std::string& d, int dir,
+                                             std::string* backend) {
+  std::lock_guard<std::mutex> lk(mu_);
+  auto si = segs_.find(s), di = segs_.find(d);
+  if (si == segs_.end() || di == segs_.end()) throw EngineError("unknown segment id");
+  auto routes = build_plan(topo_, si->second.seg, di->second.seg, dir == SPRAY_READ ? Direction::kRead : Direction::kWrite,
+                           opts_.sched.penalty, caps_);
+  if (backend) *backend = routes.front().backend;
+  std::vector<int32_t> out{1};
+  append_stream(out, routes.front().candidates);
+  return out;
+}
+
+uint64_t Engine::decompose_count(uint64_t len) const {  // scheduler.cpp:94-106
+  uint64_t n = len / opts_.sched.min_slice_size;
+  if (n == 0) n = 1;
+  if (n > opts_.sched.max_slices_per_transfer) n = opts_.sched.max_slices_per_transfer;
+  const uint64_t size = (len + n - 1) / n;
+  return (len + size - 1) / size;
+}
+
+// ------------------------------------------------------------------ batches
+
+Engine::BatchRec& Engine::batch_ref(uint64_t id) {
+  auto it = batches_.find(id);
+  if (it == batches_.end()) throw EngineError("unknown batch");
+  return it->second;
+}
+
+uint64_t Engine::allocate_batch() {
+  std::lock_guard<std::mutex> lk(mu_);
+  if (!started_) throw EngineError("engine not started");
+  for (uint32_t k = 0; k < opts_.batch_slots; ++k) {
+    const uint32_t slot = (next_slot_ + k) % opts_.batch_slots;
+    if (slot_busy_[slot]) continue;
+    slot_busy_[slot] = 1;
+    next_slot_ = slot + 1;
+    BatchRec b;
+    b.id = next_batch_++;
+    b.slot = slot;
+    b.base = reinterpret_cast<volatile BatchDev*>(bmirror_)[slot].done;
+    batches_.emplace(b.id, b);
+    return b.id;
+  }
+  throw EngineError("no free batch slot (free completed batches)");
+}
+
+static spray_batch_status_t status_of(uint64_t submitted, uint64_t done, bool failed) {
+  spray_batch_status_t st{};
+  st.remaining = submitted > done ? submitted - done : 0;
+  if (failed) {
+    st.state = SPRAY_BATCH_FAILED;
+    std::snprintf(st.failure_reason, sizeof(st.failure_reason), "AllRoutesExhausted");
+  } else {
+    st.state = st.remaining > 0 ? SPRAY_BATCH_IN_FLIGHT : SPRAY_BATCH_COMPLETE;
+  }
+  return st;
+}
+
+spray_batch_status_t Engine::batch_status(uint64_t batch) {
+  std::lock_guard<std::mutex> lk(mu_);
+  BatchRec& b = batch_ref(batch);
+  volatile BatchDev* m = &bmirror_[b.slot];
+  const uint64_t failed_id = m->failed_id;
+  const uint64_t done = m->done - b.base;
+  return status_of(b.submitted, done, failed_id == b.id);
+}
+
+spray_batch_status_t Engine::await_batch(uint64_t batch, uint64_t limit_ns) {
+  const auto t0 = std::chrono::steady_clock::now();
+  uint32_t spins = 0;
+  for (;;) {
+    spray_batch_status_t st = batch_status(batch);
+    if (st.state != SPRAY_BATCH_IN_FLIGHT) return st;
+    const uint64_t el = static_cast<uint64_t>(
+        std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now() - t0).count());
+    if (el > limit_ns) return st;
+    if (++spins < 2000) _mm_pause();
+    else std::this_thread::sleep_for(std::chrono::microseconds(20));
+  }
+}
+
+void Engine::free_batch(uint64_t batch) {
+  std::lock_guard<std::mutex> lk(mu_);
+  BatchRec& b = batch_ref(batch);
+  volatile BatchDev* m = &bmirror_[b.slot];
+  const bool failed = m->failed_id == b.id;
+  const uint64_t done = m->done - b.base;
+  if (!failed && b.submitted > 0 && done < b.submitted) throw EngineError("cannot free an in-flight batch");
+  slot_busy_[b.slot] = 0;
+  batches_.erase(batch);
+}
+
+// ------------------------------------------------------------------ submit
+
+Intent Engine::make_intent(uint64_t batch, const spray_transfer_request& req, uint64_t* n_slices) {
+  if (!started_) throw EngineError("engine not started");
+  BatchRec& b = batch_ref(batch);
+  volatile BatchDev* m = &bmirror_[b.slot];
+  if (m->failed_id == b.id) throw EngineError("batch already failed");
+  if (b.submitted > 0 && m->done - b.base >= b.submitted) throw EngineError("batch already complete");
+  auto si = segs_.find(req.src_segment ? req.src_segment : "");
+  auto di = segs_.find(req.dst_segment ? req.dst_segment : "");
+  if (si == segs_.end() || di == segs_.end()) throw EngineError("unknown segment id");
+  if (req.length == 0) throw InvalidRangeError("zero-length transfer");
+  const Buffer* sb = si->second.seg.covering(req.src_offset, req.length);
+  if (!sb) throw InvalidRangeError("source range not covered by one registered buffer");
+  const Buffer* db = di->second.seg.covering(req.dst_offset, req.length);
+  if (!db) throw InvalidRangeError("destination range not covered by one registered buffer");
+  const Direction dir = req.direction == SPRAY_READ ? Direction::kRead : Direction::kWrite;
+  const uint32_t set = set_for(si->second.seg, di->second.seg, dir);  // throws NoRouteError
+  translate(si->second);
+  translate(di->second);
+  sb = si->second.seg.covering(req.src_offset, req.length);
+  db = di->second.seg.covering(req.dst_offset, req.length);
+  Intent in{};
+  in.batch_id = b.id;
+  in.src = sb->dev_addr + (req.src_offset - sb->offset);
+  in.dst = db->dev_addr + (req.dst_offset - db->offset);
+  in.len = req.length;
+  in.hash_offset = req.src_offset;
+  in.transfer_id = next_transfer_++;
+  in.set_id = set;
+  in.batch_slot = b.slot;
+  in.flags = 0;
+  *n_slices = decompose_count(req.length);
+  return in;
+}
+
+void Engine::publish(const Intent* in, size_t n) {
+  const uint64_t cap = opts_.sub_capacity;
+  for (size_t i = 0; i < n; ++i) {
+    while (sub_tail_ - ctl_->sub_head >= cap) {
+      // ring full: make what is there visible and let the device drain it
+      std::atomic_thread_fence(std::memory_order_release);
+      ctl_->sub_tail = sub_tail_;
+      ensure_running();
+      _mm_pause();
+    }
+    ring_[sub_tail_ % cap] = in[i];
+    ++sub_tail_;
+  }
+  std::atomic_thread_fence(std::memory_order_release);
+  ctl_->sub_tail = sub_tail_;
+  ensure_running();
+}
+
+uint64_t Engine::submit_transfer(uint64_t batch, const spray_transfer_request& req) {
+  std::lock_guard<std::mutex> lk(mu_);
+  uint64_t n = 0;
+  Intent in = make_intent(batch, req, &n);
+  batch_ref(batch).submitted += n;
+  publish(&in, 1);
+  return in.transfer_id;
+}
+
+size_t Engine::submit_transfers(uint64_t batch, const spray_transfer_request* reqs, size_t n, uint64_t* ids) {
+  std::lock_guard<std::mutex> lk(mu_);
+  std::vector<Intent> v;
+  v.reserve(n);
+  size_t done = 0;
+  try {
+    for (; done < n; ++done) {
+      uint64_t k = 0;
+      v.push_back(make_intent(batch, reqs[done], &k));
+      batch_ref(batch).submitted += k;
+      if (ids) ids[done] = v.back().transfer_id;
+    }
+  } catch (...) {
+    if (!v.empty()) publish(v.data(), v.size());
+    throw;
+  }
+  publish(v.data(), v.size());
+  return done;
+}
+
+void Engine::submit_device_intents(uint64_t batch, const void* dev_intents, uint64_t n, uint64_t total_slices) {
+  std::lock_guard<std::mutex> lk(mu_);
+  BatchRec& b = batch_ref(batch);
+  b.submitted += total_slices;
+  Intent bulk{};
+  bulk.batch_id = b.id;
+  bulk.src = reinterpret_cast<uint64_t>(dev_intents);
+  bulk.len = n;
+  bulk.batch_slot = b.slot;
+  bulk.flags = kIntentBulk;
+  publish(&bulk, 1);
+}
+
+// ------------------------------------------------------------------ introspection
+
+void Engine::rail_stats(uint32_t rail, spray_rail_stats* out) {
+  if (rail >= rail_count()) throw EngineError("bad rail index");
+  std::memset(out, 0, sizeof(*out));
+  if (!rmirror_) return;
+  RailState s;
+  std::memcpy(&s, const_cast<const RailState*>(&rmirror_[rail]), sizeof(s));
+  out->bytes_posted = s.bytes_posted;
+  out->bytes_ok = s.bytes_ok;
+  out->bytes_failed = s.bytes_failed;
+  out->queue_depth = s.queued;
+  out->beta0 = s.beta0;
+  out->beta1 = s.beta1;
+  out->health = static_cast<int32_t>(s.health);
+  std::memcpy(out->latency_hist, s.hist, sizeof(s.hist));
+}
+
+void Engine::counters(uint64_t* d, uint64_t* t, uint64_t* f) {
+  if (!ctl_) {
+    *d = *t = *f = 0;
+    return;
+  }
+  *d = ctl_->bytes_dispatched;
+  *t = ctl_->bytes_terminated;
+  *f = ctl_->batches_failed;
+}
+
+void Engine::inject_fault(const std::string& rail, int effect, uint64_t start, uint64_t end, double factor) {
+  std::lock_guard<std::mutex> lk(mu_);
+  if (!started_) throw EngineError("engine not started");
+  auto r = topo_.rail_index(rail);
+  if (!r) throw ConfigError("fault schedule references unknown rail '" + rail + "'");
+  if (end <= start) throw ConfigError("fault interval must be non-empty");
+  if (effect < 0 || effect > 3) throw ConfigError("unknown fault effect");
+  if (effect != 0 && effect != 1) throw ConfigError("only down and degrade faults are emulated on hardware rails");
+  volatile FaultDev* f = &faults_[*r];
+  f->start = start;
+  f->end = end;
+  f->effect = static_cast<uint32_t>(effect);
+  f->factor = factor;
+  f->active = 1;
+  std::atomic_thread_fence(std::memory_order_seq_cst);
+  ctl_->fault_epoch = ctl_->fault_epoch + 1;
+  ctl_->heal_fault_start = 0;
+  ctl_->heal_first_ok = 0;
+}
+
+void Engine::clear_faults() {
+  std::lock_guard<std::mutex> lk(mu_);
+  if (!faults_) return;
+  for (int i = 0; i < kMaxRails; ++i) faults_[i].active = 0;
+  std::atomic_thread_fence(std::memory_order_seq_cst);
+  ctl_->fault_epoch = ctl_->fault_epoch + 1;
+}
+
+uint64_t Engine::now_ns() { return ctl_ ? ctl_->device_now : 0; }
+
+void Engine::debug_words(uint64_t* out, size_t n) {
+  std::vector<uint64_t> v;
+  if (ctl_) {
+    v = {sub_tail_, ctl_->sub_tail, ctl_->sub_head, ctl_->state, ctl_->device_now, ctl_->bytes_dispatched,
+         ctl_->bytes_terminated, ctl_->failed_attempts, ctl_->retried_ok, ctl_->trace_n,
+         static_cast<uint64_t>(cudaStreamQuery(stream_)), ctl_->prof_loops, ctl_->prof_comp_ns,
+         ctl_->prof_sub_ns, ctl_->prof_ctl_ns, ctl_->prof_n_comp, ctl_->prof_n_dec};
+    for (int q = 0; q < 8; ++q) v.push_back(static_cast<uint64_t>(ctl_->prof_x[q]));
+  }
+  for (size_t i = 0; i < n; ++i) out[i] = i < v.size() ? v[i] : 0;
+}
+
+void Engine::heal_stats(uint64_t* fs, uint64_t* ok, uint64_t* fa, uint64_t* ro) {
+  *fs = ctl_ ? ctl_->heal_fault_start : 0;
+  *ok = ctl_ ? ctl_->heal_first_ok : 0;
+  *fa = ctl_ ? ctl_->failed_attempts : 0;
+  *ro = ctl_ ? ctl_->retried_ok : 0;
+}
+
+// ------------------------------------------------------------------ trace
+
+void Engine::trace_enable(size_t cap) {
+  std::lock_guard<std::mutex> lk(mu_);
+  if (!started_) throw EngineError("engine not started");
+  ctl_->stop = 1;
+  std::atomic_thread_fence(std::memory_order_seq_cst);
+  CK(cudaStreamSynchronize(stream_));
+  ctl_->stop = 0;
+  ctl_->state = 0;
+  void* ev = nullptr;
+  void* dc = nullptr;
+  CK(cudaMalloc(&ev, cap * sizeof(spray_trace_event)));
+  CK(cudaMalloc(&dc, cap * sizeof(spray_decision)));
+  dev_allocs_.push_back(ev);
+  dev_allocs_.push_back(dc);
+  E_.trace_ev = static_cast<uint8_t*>(ev);
+  E_.trace_dec = static_cast<uint8_t*>(dc);
+  E_.trace_cap = cap;
+  trace_cap_ = cap;
+  ctl_->trace_n = 0;
+  ctl_->trace_dn = 0;
+  ctl_->trace_on = 1;
+}
+
+void Engine::trace_fetch(spray_trace_event* ev, size_t cap, size_t* n, spray_decision* dec, size_t dcap, size_t* nd) {
+  std::lock_guard<std::mutex> lk(mu_);
+  if (!started_ || !trace_cap_) throw EngineError("tracing not enabled");
+  // quiesce the kernel so the trace is complete and stable
+  ctl_->stop = 1;
+  std::atomic_thread_fence(std::memory_order_seq_cst);
+  CK(cudaStreamSynchronize(stream_));
+  ctl_->stop = 0;
+  ctl_->state = 0;
+  const uint64_t tn = std::min<uint64_t>(uint64_t(ctl_->trace_n), uint64_t(trace_cap_));
+  const uint64_t tdn = std::min<uint64_t>(uint64_t(ctl_->trace_dn), uint64_t(trace_cap_));
+  *n = ctl_->trace_n;
+  *nd = ctl_->trace_dn;
+  if (ev) CK(cudaMemcpy(ev, E_.trace_ev, std::min<uint64_t>(tn, cap) * sizeof(spray_trace_event), cudaMemcpyDeviceToHost));
+  if (dec) CK(cudaMemcpy(dec, E_.trace_dec, std::min<uint64_t>(tdn, dcap) * sizeof(spray_decision), cudaMemcpyDeviceToHost));
+}
+
+std::vector<int32_t> Engine::trace_candidates() {
+  std::lock_guard<std::mutex> lk(mu_);
+  std::vector<int32_t> out{static_cast<int32_t>(sets_.size())};
+  for (const auto& s : sets_) append_stream(out, s);
+  return out;
+}
+
+// ------------------------------------------------------------------ CE proxy
+// Copy-engine rails: the device publishes CeOrders into a mapped ring; this thread
+// issues one cudaMemcpyAsync per order on the rail's side stream, and posts the
+// completion into the mapped external-completion ring the device scheduler drains.
+void Engine::ce_proxy_loop() {
+  cudaSetDevice(device_);
+  struct Pending {
+    cudaEvent_t ev;
+    CeOrder o;
+    bool failed;
+  };
+  std::vector<Pending> pend;
+  std::vector<cudaEvent_t> pool;
+  uint64_t head[8] = {0};
+  uint64_t xc_tail = ctl_->xc_tail;
+  auto post = [&](const CeOrder& o, uint32_t status) {
+    while (xc_tail - ctl_->xc_head >= E_.xc_cap) _mm_pause();
+    volatile Completion* c = &xc_ring_[xc_tail % E_.xc_cap];
+    c->slice = o.slice;
+    c->attempt = o.attempt;
+    c->status = status;
+    c->rail = o.rail;
+    std::atomic_thread_fence(std::memory_order_release);
+    ctl_->xc_tail = ++xc_tail;
+  };
+  while (ce_run_.load()) {
+    bool any = false;
+    for (int k = 0; k < 8; ++k) {
+      while (head[k] < ctl_->ce_tail[k]) {
+        volatile CeOrder* vo = &ce_ring_[k * E_.ce_cap + (head[k] % E_.ce_cap)];
+        if (vo->stamp != head[k] + 1) break;
+        CeOrder o;
+        o.src = vo->src; o.dst = vo->dst; o.len = vo->len; o.slice = vo->slice; o.attempt = vo->attempt;
+        o.rail = vo->rail; o.ce_index = vo->ce_index; o.stamp = vo->stamp;
+        ++head[k];
+        ctl_->ce_head[k] = head[k];
+        any = true;
+        const volatile FaultDev* f = &faults_[o.rail];
+        const uint64_t now = ctl_->device_now;
+        if (f->active && f->effect == 0 && f->start <= now && now < f->end) {
+          post(o, kStFailed);
+          continue;
+        }
+        cudaEvent_t ev;
+        if (pool.empty()) {
+          cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+        } else {
+          ev = pool.back();
+          pool.pop_back();
+        }
+        cudaMemcpyAsync(reinterpret_cast<void*>(o.dst), reinterpret_cast<const void*>(o.src), o.len, cudaMemcpyDefault,
+                        ce_streams_[k]);
+        cudaEventRecord(ev, ce_streams_[k]);
+        pend.push_back(Pending{ev, o, false});
+      }
+    }
+    for (size_t i = 0; i < pend.size();) {
+      const cudaError_t q = cudaEventQuery(pend[i].ev);
+      if (q == cudaErrorNotReady) {
+        ++i;
+        continue;
+      }
+      post(pend[i].o, q == cudaSuccess ? kStOk : kStFailed);
+      pool.push_back(pend[i].ev);
+      pend[i] = pend.back();
+      pend.pop_back();
+      any = true;
+    }
+    if (!any) std::this_thread::sleep_for(std::chrono::microseconds(5));
+  }
+  for (auto& p : pend) cudaEventSynchronize(p.ev), pool.push_back(p.ev);
+  for (auto e : pool) cudaEventDestroy(e);
+}
+
+}  // namespace spray

@@ -1,0 +1,153 @@
+// engine.hpp — host side of the B200 spray engine.
+//
+// Public surface = the reference Engine's batch API (proj/include/spray/engine.hpp:90-131).
+// The host does only what must happen on the application's thread: validate the
+// request, plan the route (candidate list, cached per (src, dst, direction)), resolve
+// device-usable addresses and publish a 64-B intent into the mapped submission ring.
+// Slicing, rail choice, copies, completion accounting, retries and health all run in
+// the persistent device kernel (spray_kernel.cu). Batch status is read from mapped
+// host counters the device writes: polling a batch never touches the GPU.
+#pragma once
+#include <atomic>
+#include <cstdint>
+#include <map>
+#include <mutex>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "../../include/spray_b200.h"
+#include "dev_types.cuh"
+#include "fabric.hpp"
+#include "orchestrator.hpp"
+
+namespace spray {
+
+struct EngineOptions {
+  std::vector<std::string> backends = {"cuda"};
+  spray_sched_config sched{};
+  spray_resilience_config res{};
+  double diffusion_weight = 0.0;
+  // B200 execution parameters ("b200" section of the config document)
+  int grid = 0;                 // 0 = one CTA per SM
+  int block = 256;
+  uint64_t chunk_bytes = 128 << 10;
+  uint64_t idle_exit_ns = 20'000'000;
+  uint32_t slice_capacity = 1u << 17;
+  uint64_t work_capacity = 1ull << 21;
+  uint64_t sub_capacity = 1ull << 16;
+  uint32_t batch_slots = 1u << 16;
+  uint32_t max_sets = 1024;
+};
+
+// engine_options_from_json (engine.cpp:1199-1307): unknown keys rejected.
+EngineOptions engine_options_from_json(const std::string& text);
+void default_sched_config(spray_sched_config* c);
+void default_resilience_config(spray_resilience_config* c);
+
+class Engine {
+ public:
+  Engine(EngineOptions opts, const std::string& topology_json, int device);
+  ~Engine();
+
+  void start();
+  void stop();
+  void register_segment(const spray_segment_desc& desc);
+  uint64_t allocate_batch();
+  uint64_t submit_transfer(uint64_t batch, const spray_transfer_request& req);
+  size_t submit_transfers(uint64_t batch, const spray_transfer_request* reqs, size_t n, uint64_t* ids);
+  spray_batch_status_t batch_status(uint64_t batch);
+  spray_batch_status_t await_batch(uint64_t batch, uint64_t limit_ns);
+  void free_batch(uint64_t batch);
+
+  // Device-resident submission (bench / device producers): `dev_intents` is an HBM
+  // array of n Intent records built with make_intent(). Counts n transfers into batch.
+  spray_dev::Intent make_intent(uint64_t batch, const spray_transfer_request& req, uint64_t* n_slices);
+  void submit_device_intents(uint64_t batch, const void* dev_intents, uint64_t n, uint64_t total_slices);
+  void set_drain(bool on);
+  cudaStream_t stream() const { return stream_; }
+  bool running_kernel();
+
+  const Topology& topology() const { return topo_; }
+  uint32_t rail_count() const { return static_cast<uint32_t>(topo_.rail_count()); }
+  void rail_stats(uint32_t rail, spray_rail_stats* out);
+  void counters(uint64_t* dispatched, uint64_t* terminated, uint64_t* failed);
+  void inject_fault(const std::string& rail, int effect, uint64_t start, uint64_t end, double factor);
+  void clear_faults();
+  uint64_t now_ns();
+  void heal_stats(uint64_t* fs, uint64_t* ok, uint64_t* fa, uint64_t* ro);
+
+  void trace_enable(size_t cap);
+  void trace_fetch(spray_trace_event* ev, size_t cap, size_t* n, spray_decision* dec, size_t dcap, size_t* nd);
+  std::vector<int32_t> trace_candidates();
+  // Candidate stream of the route the engine would use (host planning only).
+  std::vector<int32_t> plan_candidates(const std::string& src, const std::string& dst, int dir,
+                                       std::string* backend);
+
+  int device() const { return device_; }
+  // Diagnostic snapshot: host/device ring positions, kernel state, counters, stream status.
+  void debug_words(uint64_t* out, size_t n);
+
+ private:
+  struct BatchRec {
+    uint64_t id = 0;
+    uint32_t slot = 0;
+    uint64_t base = 0;       // device done-counter value when the batch was allocated
+    uint64_t submitted = 0;  // slices submitted (decompose counts)
+  };
+  struct SegRec {
+    Segment seg;
+    bool translated = false;
+    std::vector<void*> registered;  // host buffers we cudaHostRegister'ed
+  };
+
+  void alloc_device();
+  void free_device();
+  void launch();
+  void ensure_running();
+  uint32_t set_for(const Segment& src, const Segment& dst, Direction dir);
+  void translate(SegRec& s);
+  void publish(const spray_dev::Intent* in, size_t n);
+  void ce_proxy_loop();
+  BatchRec& batch_ref(uint64_t id);
+  uint64_t decompose_count(uint64_t len) const;
+
+  EngineOptions opts_;
+  Topology topo_;
+  int device_;
+  std::vector<Capabilities> caps_;
+  std::mutex mu_;
+  std::map<std::string, SegRec> segs_;
+  std::map<uint64_t, BatchRec> batches_;
+  std::vector<uint8_t> slot_busy_;
+  uint64_t next_batch_ = 1, next_transfer_ = 1;
+  uint32_t next_slot_ = 0;
+  std::map<std::string, uint32_t> set_cache_;
+  std::vector<std::vector<LocalCandidate>> sets_;
+  bool started_ = false;
+
+  // device resources
+  cudaStream_t stream_ = nullptr, copy_stream_ = nullptr;
+  spray_dev::EngineDev E_{};
+  spray_dev::Control* ctl_ = nullptr;        // mapped host
+  spray_dev::Intent* ring_ = nullptr;        // mapped host
+  spray_dev::BatchDev* bmirror_ = nullptr;   // mapped host
+  spray_dev::FaultDev* faults_ = nullptr;    // mapped host
+  spray_dev::RailState* rmirror_ = nullptr;  // mapped host
+  spray_dev::CeOrder* ce_ring_ = nullptr;    // mapped host
+  spray_dev::Completion* xc_ring_ = nullptr; // mapped host
+  std::vector<void*> dev_allocs_;
+  uint64_t sub_tail_ = 0;
+  size_t trace_cap_ = 0;
+  bool drain_ = false;
+
+  // CE proxy
+  std::thread ce_thread_;
+  std::atomic<bool> ce_run_{false};
+  std::vector<cudaStream_t> ce_streams_;
+  bool has_ce_ = false;
+};
+
+}  // namespace spray

@@ -1,0 +1,485 @@
+"""Host-side mirror of the reference interface for the slice-spraying path.
+
+Same names, argument meaning and error behaviour as proj/include/spray/engine.hpp:90-131
+(Engine), proj/include/spray/backend.hpp:49-72 (TransportBackend) and
+proj/include/spray/common.hpp:31-41 (error classes). Every call goes through the C-ABI
+of libspray_b200.so; nothing here moves bytes or makes scheduling decisions.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+from dataclasses import dataclass, field
+from typing import List, Optional, Sequence
+
+import numpy as np
+
+from . import _lib as L
+
+lib = L.lib
+
+
+# ------------------------------------------------------------------ errors (common.hpp:31-41)
+class SprayError(RuntimeError):
+    pass
+
+
+class ConfigError(SprayError):
+    pass
+
+
+class EngineError(SprayError):
+    pass
+
+
+class InvalidRangeError(EngineError):
+    pass
+
+
+class NoRouteError(EngineError):
+    pass
+
+
+class CudaError(SprayError):
+    pass
+
+
+class BackendFatal(EngineError):
+    pass
+
+
+class CapabilityError(EngineError):
+    pass
+
+
+_ERRS = {-1: ConfigError, -2: EngineError, -3: InvalidRangeError, -4: NoRouteError, -5: CudaError,
+         -6: BackendFatal, -7: CapabilityError}
+
+
+def _check(rc: int):
+    if rc != 0:
+        msg = lib.spray_last_error().decode(errors="replace")
+        raise _ERRS.get(rc, SprayError)(msg)
+
+
+# ------------------------------------------------------------------ enums / records
+class Direction(enum.IntEnum):
+    READ = 0
+    WRITE = 1
+
+
+class Medium(enum.IntEnum):
+    HOST = 0
+    DEVICE = 1
+    FILE = 2
+
+
+class BatchState(enum.IntEnum):
+    IN_FLIGHT = 0
+    COMPLETE = 1
+    FAILED = 2
+
+
+class Health(enum.IntEnum):
+    HEALTHY = 0
+    EXCLUDED = 1
+    PROBING = 2
+
+
+class FaultEffect(enum.IntEnum):
+    DOWN = 0
+    DEGRADE = 1
+    JITTER = 2
+    DROP_COMPLETION = 3
+
+
+@dataclass
+class BufferDesc:
+    offset: int
+    length: int
+    data: int  # device pointer (DEVICE) or pinned host pointer (HOST)
+
+
+@dataclass
+class SegmentDescriptor:
+    id: str
+    medium: Medium
+    node: str
+    buffers: List[BufferDesc]
+    device: str = ""
+
+
+@dataclass
+class TransferRequest:
+    src_segment: str
+    src_offset: int
+    dst_segment: str
+    dst_offset: int
+    length: int
+    direction: Direction = Direction.WRITE
+
+
+@dataclass
+class BatchStatus:
+    state: BatchState
+    remaining: int
+    failure_reason: str = ""
+
+
+@dataclass
+class RailStats:
+    rail_id: str
+    bytes_posted: int
+    bytes_ok: int
+    bytes_failed: int
+    queue_depth: int
+    beta0: float
+    beta1: float
+    health: Health
+    latency_hist: List[int] = field(default_factory=list)
+
+
+def _seg_c(d: SegmentDescriptor):
+    bufs = (L.BufferDescC * len(d.buffers))(*[L.BufferDescC(b.offset, b.length, b.data) for b in d.buffers])
+    s = L.SegmentDescC(d.id.encode(), int(d.medium), d.node.encode(), bufs, len(d.buffers),
+                       (d.device or "").encode())
+    return s, bufs
+
+
+def _req_c(r: TransferRequest):
+    return L.TransferRequestC(r.src_segment.encode(), r.src_offset, r.dst_segment.encode(), r.dst_offset,
+                              r.length, int(r.direction))
+
+
+def _reqs_c(reqs: Sequence[TransferRequest]):
+    keep = []
+    arr = (L.TransferRequestC * len(reqs))()
+    for i, r in enumerate(reqs):
+        s, d = r.src_segment.encode(), r.dst_segment.encode()
+        keep += [s, d]
+        arr[i] = L.TransferRequestC(s, r.src_offset, d, r.dst_offset, r.length, int(r.direction))
+    return arr, keep
+
+
+def _status(st: L.BatchStatusC) -> BatchStatus:
+    return BatchStatus(BatchState(st.state), int(st.remaining), st.failure_reason.decode())
+
+
+# ------------------------------------------------------------------ Engine
+class Engine:
+    """spray::Engine (engine.hpp:90-131) on one B200. `topology` is the reference JSON
+    topology document; `config` the engine config document (unknown keys rejected)."""
+
+    def __init__(self, topology: str, config: Optional[str] = None, device: int = 0):
+        h = C.c_void_p()
+        _check(lib.spray_engine_create(config.encode() if config else None, topology.encode(), device,
+                                       C.byref(h)))
+        self._h = h
+        self.device = device
+        self._keep = []
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib.spray_engine_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        self.start()
+        return self
+
+    def __exit__(self, *exc):
+        self.stop()
+        self.close()
+
+    def start(self):
+        _check(lib.spray_engine_start(self._h))
+
+    def stop(self):
+        _check(lib.spray_engine_stop(self._h))
+
+    def register_segment(self, desc: SegmentDescriptor):
+        s, bufs = _seg_c(desc)
+        _check(lib.spray_register_segment(self._h, C.byref(s)))
+
+    def allocate_batch(self) -> int:
+        b = C.c_uint64()
+        _check(lib.spray_allocate_batch(self._h, C.byref(b)))
+        return b.value
+
+    def submit_transfer(self, batch: int, req: TransferRequest) -> int:
+        r = _req_c(req)
+        t = C.c_uint64()
+        _check(lib.spray_submit_transfer(self._h, batch, C.byref(r), C.byref(t)))
+        return t.value
+
+    def submit_transfers(self, batch: int, reqs: Sequence[TransferRequest]) -> List[int]:
+        arr, keep = _reqs_c(reqs)
+        ids = (C.c_uint64 * max(1, len(reqs)))()
+        done = C.c_size_t()
+        _check(lib.spray_submit_transfers(self._h, batch, arr, len(reqs), ids, C.byref(done)))
+        return list(ids[: done.value])
+
+    def batch_status(self, batch: int) -> BatchStatus:
+        st = L.BatchStatusC()
+        _check(lib.spray_batch_status(self._h, batch, C.byref(st)))
+        return _status(st)
+
+    def await_batch(self, batch: int, limit_ns: int = 120_000_000_000) -> BatchStatus:
+        st = L.BatchStatusC()
+        _check(lib.spray_await_batch(self._h, batch, limit_ns, C.byref(st)))
+        return _status(st)
+
+    def free_batch(self, batch: int):
+        _check(lib.spray_free_batch(self._h, batch))
+
+    # ---- device-resident submission
+    def prepare_transfers(self, reqs: Sequence[TransferRequest]) -> "Prepared":
+        arr, keep = _reqs_c(reqs)
+        p = C.c_void_p()
+        _check(lib.spray_prepare_transfers(self._h, arr, len(reqs), C.byref(p)))
+        return Prepared(self, p)
+
+    # ---- introspection
+    def rail_count(self) -> int:
+        n = C.c_uint32()
+        _check(lib.spray_rail_count(self._h, C.byref(n)))
+        return n.value
+
+    def rail_id(self, r: int) -> str:
+        buf = C.create_string_buffer(256)
+        _check(lib.spray_rail_id(self._h, r, buf, 256))
+        return buf.value.decode()
+
+    def rail_stats(self, r: int) -> RailStats:
+        s = L.RailStatsC()
+        _check(lib.spray_rail_stats_get(self._h, r, C.byref(s)))
+        return RailStats(self.rail_id(r), s.bytes_posted, s.bytes_ok, s.bytes_failed, s.queue_depth, s.beta0,
+                         s.beta1, Health(s.health), list(s.latency_hist))
+
+    def counters(self):
+        d, t, f = C.c_uint64(), C.c_uint64(), C.c_uint64()
+        _check(lib.spray_engine_counters(self._h, C.byref(d), C.byref(t), C.byref(f)))
+        return {"bytes_dispatched": d.value, "bytes_terminated": t.value, "batches_failed": f.value}
+
+    def inject_fault(self, rail_id: str, effect: FaultEffect, start_ns: int, end_ns: int, factor: float = 1.0):
+        _check(lib.spray_inject_fault(self._h, rail_id.encode(), int(effect), start_ns, end_ns, factor))
+
+    def clear_faults(self):
+        _check(lib.spray_clear_faults(self._h))
+
+    def now_ns(self) -> int:
+        return int(lib.spray_engine_now_ns(self._h))
+
+    def heal_stats(self):
+        a, b, c, d = (C.c_uint64() for _ in range(4))
+        _check(lib.spray_heal_stats(self._h, C.byref(a), C.byref(b), C.byref(c), C.byref(d)))
+        return {"fault_start_ns": a.value, "first_reroute_ok_ns": b.value, "failed_attempts": c.value,
+                "retried_ok": d.value}
+
+    # ---- trace (slice-plan parity)
+    def trace_enable(self, capacity: int = 1 << 20):
+        _check(lib.spray_trace_enable(self._h, capacity))
+
+    def trace_fetch(self, cap: int = 1 << 20):
+        from .trace import EVENT_DTYPE, DECISION_DTYPE
+        ev = np.zeros(cap, EVENT_DTYPE)
+        dec = np.zeros(cap, DECISION_DTYPE)
+        n, nd = C.c_size_t(), C.c_size_t()
+        _check(lib.spray_trace_fetch(self._h, ev.ctypes.data, cap, C.byref(n), dec.ctypes.data, cap,
+                                     C.byref(nd)))
+        if n.value > cap or nd.value > cap:
+            raise EngineError(f"trace overflow: {n.value} events / {nd.value} decisions > capacity {cap}")
+        return ev[: n.value].copy(), dec[: nd.value].copy()
+
+    def trace_candidates(self) -> np.ndarray:
+        n = C.c_size_t()
+        _check(lib.spray_trace_candidates(self._h, None, 0, C.byref(n)))
+        out = np.zeros(n.value, np.int32)
+        _check(lib.spray_trace_candidates(self._h, out.ctypes.data, n.value, C.byref(n)))
+        return out
+
+    def plan_candidates(self, src: str, dst: str, direction: Direction = Direction.WRITE):
+        n = C.c_size_t()
+        b = C.create_string_buffer(64)
+        _check(lib.spray_plan_candidates(self._h, src.encode(), dst.encode(), int(direction), None, 0,
+                                         C.byref(n), b, 64))
+        out = np.zeros(n.value, np.int32)
+        _check(lib.spray_plan_candidates(self._h, src.encode(), dst.encode(), int(direction), out.ctypes.data,
+                                         n.value, C.byref(n), b, 64))
+        return out, b.value.decode()
+
+
+class Prepared:
+    """Intents planned once and staged in HBM; run() submits them into a batch and times
+    the drain-mode engine launch with CUDA events on the engine stream."""
+
+    def __init__(self, eng: Engine, h):
+        self.eng, self._h = eng, h
+
+    def run(self, batch: int) -> float:
+        ms = C.c_float()
+        _check(lib.spray_run_prepared(self.eng._h, batch, self._h, C.byref(ms)))
+        return ms.value
+
+    def free(self):
+        if self._h:
+            lib.spray_prepared_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        self.free()
+
+
+# ------------------------------------------------------------------ TransportBackend (plugin mode)
+@dataclass
+class SliceWorkRequest:  # backend.hpp:15-27
+    slice: int
+    batch: int
+    src_segment: str
+    src_offset: int
+    dst_segment: str
+    dst_offset: int
+    length: int
+    direction: Direction = Direction.WRITE
+    local_rail: int = 0
+    remote_rail: int = 0xFFFFFFFF
+    attempt: int = 0
+
+
+@dataclass
+class CompletionEvent:  # backend.hpp:33-40
+    slice: int
+    batch: int
+    status: int
+    rail: int
+    t_obs: int
+    bytes: int
+
+
+@dataclass
+class PostResult:  # backend.hpp:44-47
+    accepted: int
+    fatal: bool = False
+
+
+def hash128(s: str):
+    """common.hpp:111-120 two-lane FNV-1a."""
+    def fnv(data: bytes, h: int) -> int:
+        for b in data:
+            h = ((h ^ b) * 0x100000001B3) & 0xFFFFFFFFFFFFFFFF
+        return h
+    d = s.encode()
+    return fnv(d, 0xCBF29CE484222325), fnv(d, 0x84222325CBF29CE4)
+
+
+class CudaBackend:
+    """TransportBackend over CUDA (the insertion point the reference's load_backends,
+    engine.cpp:116-140, would bind as "cuda")."""
+
+    def __init__(self, device: int = 0):
+        h = C.c_void_p()
+        _check(lib.spray_backend_open(device, C.byref(h)))
+        self._h = h
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib.spray_backend_close(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def start(self):
+        _check(lib.spray_backend_start(self._h))
+
+    def stop(self):
+        _check(lib.spray_backend_stop(self._h))
+
+    def capabilities(self) -> L.BackendCaps:
+        c = L.BackendCaps()
+        _check(lib.spray_backend_capabilities(self._h, C.byref(c)))
+        return c
+
+    def attach_segment_metadata(self, desc: SegmentDescriptor) -> Optional[bytes]:
+        s, bufs = _seg_c(desc)
+        blob = C.create_string_buffer(256)
+        n = C.c_size_t()
+        rc = lib.spray_backend_attach_segment(self._h, C.byref(s), blob, 256, C.byref(n))
+        if rc == -7:
+            return None
+        _check(rc)
+        return blob.raw[: n.value]
+
+    def post_slices(self, reqs: Sequence[SliceWorkRequest]) -> PostResult:
+        arr = (L.SliceWR * len(reqs))()
+        for i, r in enumerate(reqs):
+            slo, shi = hash128(r.src_segment)
+            dlo, dhi = hash128(r.dst_segment)
+            arr[i] = L.SliceWR(r.slice, r.batch, slo, shi, r.src_offset, dlo, dhi, r.dst_offset, r.length,
+                               int(r.direction), r.local_rail, r.remote_rail, r.attempt)
+        acc = C.c_size_t()
+        rc = lib.spray_backend_post(self._h, arr, len(reqs), C.byref(acc))
+        if rc == -6:
+            return PostResult(0, True)
+        _check(rc)
+        return PostResult(acc.value, False)
+
+    def poll_completions(self, max_events: int = 32) -> List[CompletionEvent]:
+        arr = (L.CQE * max_events)()
+        n = C.c_size_t()
+        _check(lib.spray_backend_poll(self._h, arr, max_events, C.byref(n)))
+        return [CompletionEvent(c.slice, c.batch, c.status, c.rail, c.t_obs_ns, c.bytes) for c in arr[: n.value]]
+
+    def fatal(self) -> bool:
+        return bool(lib.spray_backend_fatal(self._h))
+
+    def latch_fatal(self):
+        lib.spray_backend_latch_fatal(self._h)
+
+
+# ------------------------------------------------------------------ utilities
+def fill_splitmix(device: int, ptr: int, n: int, seed: int):
+    """Device fill with the reference payload generator (bench.cpp:59-67)."""
+    _check(lib.spray_fill_splitmix(device, ptr, n, seed))
+
+
+def checksum(device: int, ptr: int, n: int) -> int:
+    out = C.c_uint64()
+    _check(lib.spray_checksum(device, ptr, n, C.byref(out)))
+    return out.value
+
+
+def host_alloc(n: int) -> int:
+    p = C.c_void_p()
+    _check(lib.spray_host_alloc(n, C.byref(p)))
+    return p.value
+
+
+def host_free(p: int):
+    _check(lib.spray_host_free(p))
+
+
+def ipc_export(device: int, ptr: int) -> bytes:
+    buf = (C.c_uint8 * 64)()
+    _check(lib.spray_ipc_export(device, ptr, buf))
+    return bytes(buf)
+
+
+def ipc_open(device: int, handle: bytes) -> int:
+    buf = (C.c_uint8 * 64).from_buffer_copy(handle)
+    p = C.c_void_p()
+    _check(lib.spray_ipc_open(device, buf, C.byref(p)))
+    return p.value
+
+
+def ipc_close(ptr: int):
+    _check(lib.spray_ipc_close(ptr))
