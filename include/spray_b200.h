@@ -217,10 +217,15 @@ int spray_plan_candidates(spray_engine* e, const char* src_segment, const char* 
  *   RESET(now=t_ns)                    periodic_reset(now)                 (scheduler.cpp:232-240)
  *   RESET_RAIL(rail, now=t_ns)         reset_rail                          (scheduler.cpp:242-247)
  *   EXPECT_HEALTH(rail, state=flags)   assertion: health(rail) == state
+ *   DUE_PROBES(now=t_ns)               due_probes(now): excluded rails whose timer
+ *                                      elapsed go to PROBING       (resilience.cpp:220-244)
+ *   PROBE_DONE(rail, len, status, now=now_ns)  release(rail,len); observe_probe(rail,
+ *                                      status, now)                (resilience.cpp:191-212)
  */
 enum spray_trace_kind {
   SPRAY_EV_DECIDE = 1, SPRAY_EV_COMPLETE = 2, SPRAY_EV_CHARGE = 3, SPRAY_EV_RELEASE = 4,
-  SPRAY_EV_HEALTH = 5, SPRAY_EV_RESET = 6, SPRAY_EV_RESET_RAIL = 7, SPRAY_EV_EXPECT_HEALTH = 8
+  SPRAY_EV_HEALTH = 5, SPRAY_EV_RESET = 6, SPRAY_EV_RESET_RAIL = 7, SPRAY_EV_EXPECT_HEALTH = 8,
+  SPRAY_EV_DUE_PROBES = 9, SPRAY_EV_PROBE_DONE = 10
 };
 #define SPRAY_EVF_MODEL 0x1u
 #define SPRAY_EVF_CANCELLED 0x2u

@@ -29,6 +29,7 @@ DECISION_DTYPE = np.dtype([
 assert EVENT_DTYPE.itemsize == 64 and DECISION_DTYPE.itemsize == 32
 
 EV_DECIDE, EV_COMPLETE, EV_CHARGE, EV_RELEASE, EV_HEALTH, EV_RESET, EV_RESET_RAIL, EV_EXPECT = range(1, 9)
+EV_DUE_PROBES, EV_PROBE_DONE = 9, 10
 EVF_MODEL, EVF_CANCELLED = 1, 2
 NO_RAIL = 0xFFFFFFFF
 

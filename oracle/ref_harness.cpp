@@ -276,6 +276,15 @@ int ref_replay(const char* topo, const spray_sched_config* sc, const spray_resil
         case SPRAY_EV_EXPECT_HEALTH:
           if (static_cast<uint32_t>(sched.health(e.rail)) != e.flags) ++bad;
           break;
+        case SPRAY_EV_DUE_PROBES: (void)res.due_probes(e.t_ns); break;
+        case SPRAY_EV_PROBE_DONE: {
+          const int status = static_cast<int>((e.flags >> 8) & 0xff);
+          sched.release(e.rail, e.len);
+          res.observe_probe(e.rail, status == 0 ? SliceStatus::kOk : status == 1 ? SliceStatus::kFailed
+                                                                                   : SliceStatus::kTimeout,
+                            e.now_ns);
+          break;
+        }
         default: g_err = "bad event kind"; return -1;
       }
     }

@@ -289,6 +289,48 @@ void so_observe(so_sched* s, uint32_t local, uint32_t remote, int status, double
   }
 }
 
+/* resilience.cpp:150-160 reintegrate */
+static void so_reintegrate(so_sched* s, uint32_t rail, uint64_t now) {
+  s->rails[rail].health = SPRAY_HEALTHY;
+  so_reset_rail(s, rail, now);
+  so_res_rail* r = &s->res[rail];
+  r->consec_failures = 0;
+  r->degradation_count = 0;
+  r->probe_streak = 0;
+  r->backoff = 0;
+}
+
+/* resilience.cpp:191-212 observe_probe */
+void so_observe_probe(so_sched* s, uint32_t rail, int status, uint64_t now) {
+  so_res_rail* r = &s->res[rail];
+  r->probe_inflight = 0;
+  if (s->rails[rail].health == SPRAY_HEALTHY) return;
+  if (status == SPRAY_SLICE_OK) {
+    r->probe_streak++;
+    if (r->probe_streak >= s->rcfg.probe_successes_needed)
+      so_reintegrate(s, rail, now);
+    else
+      r->next_probe = now;
+  } else {
+    if (s->rails[rail].health != SPRAY_EXCLUDED) s->rails[rail].health = SPRAY_EXCLUDED;
+    r->probe_streak = 0;
+    r->backoff = r->backoff + 1 < s->rcfg.probe_backoff_cap ? r->backoff + 1 : s->rcfg.probe_backoff_cap;
+    r->next_probe = now + backoff_interval(s, r->backoff);
+  }
+}
+
+/* resilience.cpp:220-244 due_probes (the partner choice does not touch scheduler state) */
+void so_due_probes(so_sched* s, uint64_t now) {
+  for (uint32_t i = 0; i < s->n_rails; ++i) {
+    const int h = s->rails[i].health;
+    if (h == SPRAY_HEALTHY) continue;
+    if (s->res[i].probe_inflight) continue;
+    if (s->res[i].next_probe > now) continue;
+    s->res[i].probe_inflight = 1;
+    if (h == SPRAY_EXCLUDED) s->rails[i].health = SPRAY_PROBING;
+  }
+}
+
 /* ------------------------------------------------------------- replay */
 
 int so_parse_candidates(const int32_t* st, size_t len, so_cset* sets, uint32_t max_sets,
@@ -362,6 +404,11 @@ int so_replay(so_sched* s, const so_cset* sets, uint32_t n_sets, const spray_tra
       case SPRAY_EV_RESET_RAIL: so_reset_rail(s, e->rail, e->t_ns); break;
       case SPRAY_EV_EXPECT_HEALTH:
         if (s->rails[e->rail].health != (int)e->flags) ++bad;
+        break;
+      case SPRAY_EV_DUE_PROBES: so_due_probes(s, e->t_ns); break;
+      case SPRAY_EV_PROBE_DONE:
+        so_release(s, e->rail, e->len);
+        so_observe_probe(s, e->rail, (int)((e->flags >> 8) & 0xff), e->now_ns);
         break;
       default: return -1;
     }

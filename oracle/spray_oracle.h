@@ -92,6 +92,10 @@ void so_reset_rail(so_sched* s, uint32_t rail, uint64_t now);/* 242-247 */
 void so_observe(so_sched* s, uint32_t local, uint32_t remote, int status, double t_obs_s,
                 double predicted_s, uint64_t now);
 
+/* resilience.cpp:191-212, 220-244 */
+void so_observe_probe(so_sched* s, uint32_t rail, int status, uint64_t now);
+void so_due_probes(so_sched* s, uint64_t now);
+
 /* Parse a flattened candidate stream (spray_b200.h). Returns number of sets or -1.
  * Storage for cands/pairs is carved from the caller's arrays. */
 int so_parse_candidates(const int32_t* stream, size_t len, so_cset* sets, uint32_t max_sets,

@@ -304,6 +304,10 @@ int spray_replay_device(int device, const spray_sched_config* sc, const spray_re
       E.degradation_events = rc->degradation_events;
       E.degradation_ratio = rc->degradation_ratio;
       E.degradation_min_t = rc->degradation_min_t_obs_s;
+      E.probe_successes = rc->probe_successes_needed;
+      E.probe_interval = rc->probe_interval_ns;
+      E.probe_backoff_mult = rc->probe_backoff_mult;
+      E.probe_backoff_cap = rc->probe_backoff_cap;
       CK(cudaMemcpy(const_cast<RailDesc*>(E.rails), rd.data(), sizeof(RailDesc) * n_rails, cudaMemcpyHostToDevice));
       CK(cudaMemcpy(E.rail_state, rs.data(), sizeof(RailState) * n_rails, cudaMemcpyHostToDevice));
       if (!sets.empty())

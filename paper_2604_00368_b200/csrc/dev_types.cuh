@@ -30,7 +30,8 @@ struct RailDesc {
   int32_t gpu;            // owning GPU ordinal (-1 for host-side rails)
   int32_t via;            // relay GPU (relay rails)
   uint32_t ce_index;      // CE proxy stream index (CE rails)
-  uint32_t pad_[2];
+  uint8_t n_partners;     // probe counterparts, affinity partner first (resilience.cpp:17-44)
+  uint8_t partners[15];
 };
 
 // Scheduler cost state (scheduler.hpp:158-168) + resilience record (resilience.hpp:68-76)
@@ -46,6 +47,8 @@ struct RailState {
   int32_t degradation_count;
   int32_t backoff;
   int32_t probe_streak;
+  uint32_t probe_inflight;
+  uint32_t pad_;
   uint64_t next_probe, excluded_at;
   uint64_t bytes_posted, bytes_ok, bytes_failed;
   uint32_t hist[48];
@@ -95,8 +98,10 @@ struct Slice {
   uint32_t target;         // slot chunk counter value once this attempt's chunks are done
   uint32_t n_failed_pairs;
   uint8_t failed_local[4], failed_remote[4];  // burned pairs (engine.cpp:765-767)
-  uint8_t pad_[24];
+  uint32_t kind;           // kSliceData or kSliceProbe (engine.hpp:133 SliceKind)
+  uint8_t pad_[20];
 };
+constexpr uint32_t kSliceData = 0, kSliceProbe = 2;
 static_assert(sizeof(Slice) == 128, "slice record is 128 B");
 
 // SM work item: one chunk, self-contained so a worker never reads the slice record to
@@ -221,6 +226,10 @@ struct EngineDev {
   double degradation_ratio, degradation_min_t;
   uint32_t max_attempts;
   uint32_t has_ce;                             // poll the CE proxy completion ring
+  uint64_t probe_interval, probe_bytes;        // resilience.hpp:23-26
+  double probe_backoff_mult;
+  int32_t probe_backoff_cap, pad_pb_;
+  uint64_t scratch;                            // HBM probe scratch (2 x probe_bytes)
   uint64_t chunk_bytes;                        // SM work granule (power of two)
   uint32_t chunk_shift;                        // log2(chunk_bytes)
   uint32_t pad_cs_;

@@ -272,6 +272,29 @@ void Engine::alloc_device() {
     rd[i].gpu = r.gpu;
     rd[i].via = r.via;
     rd[i].ce_index = r.ce_index;
+    // probe counterparts (resilience.cpp:17-44): same-backend rails on other nodes, the
+    // 1:1 affinity partner first, nodes in id order; node-local backends probe themselves
+    {
+      const auto& own = topo_.rails_on(r.node, r.backend);
+      size_t my_pos = 0;
+      for (size_t k = 0; k < own.size(); ++k)
+        if (own[k] == i) my_pos = k;
+      std::vector<std::string> others;
+      for (const NodeDecl& n : topo_.nodes())
+        if (n.id != r.node && !topo_.rails_on(n.id, r.backend).empty()) others.push_back(n.id);
+      std::sort(others.begin(), others.end());
+      std::vector<uint32_t> ps;
+      for (const std::string& n : others) {
+        const auto& theirs = topo_.rails_on(n, r.backend);
+        const uint32_t first = theirs[my_pos % theirs.size()];
+        ps.push_back(first);
+        for (uint32_t t : theirs)
+          if (t != first) ps.push_back(t);
+      }
+      if (ps.empty()) ps.push_back(i);
+      rd[i].n_partners = static_cast<uint8_t>(std::min<size_t>(ps.size(), 15));
+      for (size_t k = 0; k < rd[i].n_partners; ++k) rd[i].partners[k] = static_cast<uint8_t>(ps[k]);
+    }
     rs[i] = RailState{};
     rs[i].beta0 = opts_.sched.beta0_init_s;  // scheduler.cpp:87-90
     rs[i].beta1 = opts_.sched.beta1_init;
@@ -337,6 +360,11 @@ void Engine::alloc_device() {
   E_.degradation_ratio = opts_.res.degradation_ratio;
   E_.degradation_min_t = opts_.res.degradation_min_t_obs_s;
   E_.max_attempts = opts_.res.max_attempts;
+  E_.probe_interval = opts_.res.probe_interval_ns;
+  E_.probe_bytes = std::min<uint64_t>(opts_.res.probe_bytes, 1ull << 20);
+  E_.probe_backoff_mult = opts_.res.probe_backoff_mult;
+  E_.probe_backoff_cap = opts_.res.probe_backoff_cap;
+  E_.scratch = reinterpret_cast<uint64_t>(dev(2 * E_.probe_bytes));
   E_.chunk_bytes = opts_.chunk_bytes;
   E_.chunk_shift = 0;
   while ((1ull << E_.chunk_shift) < opts_.chunk_bytes) ++E_.chunk_shift;

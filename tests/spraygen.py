@@ -10,8 +10,9 @@ import json
 
 import numpy as np
 
-from oracle.oracle import (EV_CHARGE, EV_COMPLETE, EV_DECIDE, EV_EXPECT, EV_HEALTH, EV_RELEASE,
-                           EV_RESET, EV_RESET_RAIL, EVENT_DTYPE, EVF_CANCELLED, EVF_MODEL, NO_RAIL)
+from oracle.oracle import (EV_CHARGE, EV_COMPLETE, EV_DECIDE, EV_DUE_PROBES, EV_EXPECT, EV_HEALTH,
+                           EV_PROBE_DONE, EV_RELEASE, EV_RESET, EV_RESET_RAIL, EVENT_DTYPE, EVF_CANCELLED,
+                           EVF_MODEL, NO_RAIL)
 
 SIM_CAPS = dict(pairs="all", cross=True, same=False)          # sim_backend.cpp:96-113
 MEMORY_CAPS = dict(pairs="all", cross=True, same=True)        # memory_backend.cpp:8-19
@@ -53,6 +54,7 @@ def random_trace(rng: np.random.Generator, cstate, n_sets: int, n_rails: int, bw
     (oracle.CState) is stepped alongside so completions release what was charged."""
     events = []
     outstanding = []   # (local, remote, len, predicted, x, model)
+    probes = []        # rails with a probe in flight
     now = 0
     for _ in range(n_events):
         now += int(rng.integers(1_000, 200_000))
@@ -96,10 +98,35 @@ def random_trace(rng: np.random.Generator, cstate, n_sets: int, n_rails: int, bw
                 events.append(e[0])
                 e = c
                 outstanding.append((r, NO_RAIL, ln, 0.0, 0.0, False))
-        elif u < 0.90 and health_changes:
+        elif u < 0.88 and health_changes:
             e["kind"] = EV_HEALTH
             e["rail"] = int(rng.integers(0, n_rails))
-            e["flags"] = int(rng.choice([0, 0, 1, 2]))
+            e["flags"] = int(rng.choice([0, 0, 1]))
+            cstate.step(e)
+        elif u < 0.90 and health_changes:
+            # prober: due_probes(now) moves due excluded rails to PROBING; each gets a
+            # probe slice (charged) whose completion runs observe_probe
+            before = cstate.step(np.zeros(0, EVENT_DTYPE))[3].copy()
+            e["kind"] = EV_DUE_PROBES
+            e["t_ns"] = now + int(rng.integers(0, 3)) * 1_000_000_000
+            _, _, _, health, _ = cstate.step(e)
+            events.append(e[0])
+            for r in np.nonzero((health == 2) & (before == 1))[0]:
+                c = np.zeros(1, EVENT_DTYPE)
+                c["kind"] = EV_CHARGE
+                c["rail"] = int(r)
+                c["len"] = 4096
+                cstate.step(c)
+                events.append(c[0])
+                probes.append(int(r))
+            continue
+        elif u < 0.91 and probes:
+            r = probes.pop(int(rng.integers(0, len(probes))))
+            e["kind"] = EV_PROBE_DONE
+            e["rail"] = r
+            e["len"] = 4096
+            e["flags"] = (0 if rng.random() < 0.7 else 1) << 8
+            e["now_ns"] = now
             cstate.step(e)
         elif u < 0.93 and resets:
             e["kind"] = EV_RESET

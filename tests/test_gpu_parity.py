@@ -1,0 +1,376 @@
+"""Parity of the CUDA path (libspray_b200.so on a B200) with the oracle and the reference.
+
+* Device decision function (replay kernel) vs reference-recorded decisions: bit-exact.
+* Live engine traces replayed through the C oracle and the device replay: identical plans.
+* Config 1 (64 MiB over 2 rails): plan identical to the reference's, delivered bytes equal
+  to the reference engine's delivered bytes (checksum).
+* Delivered bytes bit-exact for random intents, KV batches, faults and retries.
+"""
+import ctypes as C
+import json
+import os
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+import paper_2604_00368_b200 as sp  # noqa: E402
+from paper_2604_00368_b200 import _lib, fabrics, trace  # noqa: E402
+from oracle.oracle import COracle, ResConfig, SchedConfig, res_config, sched_config  # noqa: E402
+
+DEV = 0
+
+
+def _cfg_c(sc):
+    return _lib.SchedConfig.from_buffer_copy(bytes(sc))
+
+
+def _rcfg_c(rc):
+    return _lib.ResConfig.from_buffer_copy(bytes(rc))
+
+
+@pytest.fixture(scope="module")
+def co():
+    return COracle()
+
+
+def dev_buf(n, fill_seed=None):
+    t = torch.zeros(max(n, 1), dtype=torch.uint8, device=f"cuda:{DEV}")
+    if fill_seed is not None:
+        sp.fill_splitmix(DEV, t.data_ptr(), n, fill_seed)
+    return t
+
+
+# ------------------------------------------------------------------ device decision function
+def test_device_replay_matches_reference_goldens(golden_dir):
+    z = np.load(os.path.join(golden_dir, "replay.npz"))
+    cases = sorted({k.split("__")[0] for k in z.files})
+    for c in cases:
+        sc = _cfg_c(SchedConfig.from_buffer_copy(z[c + "__sc"].tobytes()))
+        rc = _rcfg_c(ResConfig.from_buffer_copy(z[c + "__rc"].tobytes()))
+        dec, bad = trace.replay_device(DEV, sc, rc, z[c + "__bw"], z[c + "__tier"], z[c + "__rank"],
+                                       z[c + "__stream"], z[c + "__events"])
+        assert dec.tobytes() == z[c + "__decisions"].tobytes(), c
+        assert bad == 0
+
+
+def test_fill_and_checksum_match_oracle(co):
+    for n in (1, 7, 8, 4099, 1 << 20, (1 << 20) + 3):
+        t = dev_buf(n, fill_seed=1234)
+        host = t.cpu().numpy()[:n]
+        assert np.array_equal(host, co.fill(n, 1234))
+        assert sp.checksum(DEV, t.data_ptr(), n) == co.checksum(host)
+
+
+# ------------------------------------------------------------------ engine helpers
+def make_engine(topo, cfg=None):
+    e = sp.Engine(topo, json.dumps(cfg or {}), DEV)
+    e.start()
+    return e
+
+
+def replay_live(co, e, sc, rc, bw, tier, rank):
+    ev, dec = e.trace_fetch(1 << 20)
+    cand = e.trace_candidates()
+    ref = co.replay(sc, rc, bw, tier, rank, cand, ev)
+    assert ref["decisions"].tobytes() == dec.tobytes()
+    assert ref["expect_failures"] == 0
+    ddec, bad = trace.replay_device(DEV, _cfg_c(sc), _rcfg_c(rc), bw, tier, rank, cand, ev)
+    assert ddec.tobytes() == dec.tobytes() and bad == 0
+    return ev, dec
+
+
+def rails_of(topo):
+    doc = json.loads(topo)
+    ids = [r["id"] for r in doc["rails"]]
+    order = sorted(range(len(ids)), key=lambda i: ids[i])
+    rank = [0] * len(ids)
+    for k, i in enumerate(order):
+        rank[i] = k
+    aff = {"direct": 1, "same_socket": 2, "cross_socket": 3}
+    return ([float(r["bandwidth_bytes_per_sec"]) for r in doc["rails"]], [aff[r["affinity"]] for r in doc["rails"]],
+            rank)
+
+
+# ------------------------------------------------------------------ config 1
+def test_config1_plan_and_bytes_match_reference(co, golden_dir):
+    z = np.load(os.path.join(golden_dir, "c1.npz"))
+    topo = fabrics.two_node(2, 1e9, backend="cuda")
+    e = make_engine(topo, {"backends": ["cuda"]})
+    e.trace_enable(1 << 16)
+    n = 64 << 20
+    src = dev_buf(n, fill_seed=1 ^ 0x517CC1B727220A95)  # bench.cpp:99 payload, seed 1
+    dst = dev_buf(n)
+    e.register_segment(sp.SegmentDescriptor("bench/src", sp.Medium.DEVICE, "a", [sp.BufferDesc(0, n, src.data_ptr())]))
+    e.register_segment(sp.SegmentDescriptor("bench/dst", sp.Medium.DEVICE, "b", [sp.BufferDesc(0, n, dst.data_ptr())]))
+    b = e.allocate_batch()
+    e.submit_transfer(b, sp.TransferRequest("bench/src", 0, "bench/dst", 0, n))
+    st = e.await_batch(b, 30_000_000_000)
+    assert st.state == sp.BatchState.COMPLETE and st.remaining == 0
+    assert sp.checksum(DEV, dst.data_ptr(), n) == int(z["dst_checksum"])
+    ev, dec = e.trace_fetch(1 << 16)
+    g = z["decisions"]
+    assert np.array_equal(dec["local"], g["local"]) and np.array_equal(dec["remote"], g["remote"])
+    assert dec.tobytes() == g.tobytes()
+    c = e.counters()
+    assert c["bytes_dispatched"] == c["bytes_terminated"] == n
+    e.stop()
+
+
+# ------------------------------------------------------------------ live trace parity
+@pytest.mark.parametrize("policy", ["telemetry", "rr", "hash"])
+def test_live_trace_replays_identically(co, policy):
+    bws = [4e9, 2e9, 1e9, 1e9]
+    topo = fabrics.two_node(4, bws, backend="cuda", affinities=["direct", "direct", "same_socket", "direct"])
+    sc = sched_config(policy={"telemetry": 0, "rr": 1, "hash": 2}[policy])
+    e = make_engine(topo, {"scheduler": {"policy": policy}, "resilience": {"degradation_ratio": 1e9},
+                           "b200": {"chunk_bytes": 65536}})
+    e.trace_enable(1 << 18)
+    n = 96 << 20
+    src = dev_buf(n, fill_seed=5)
+    dst = dev_buf(n)
+    e.register_segment(sp.SegmentDescriptor("s", sp.Medium.DEVICE, "a", [sp.BufferDesc(0, n, src.data_ptr())]))
+    e.register_segment(sp.SegmentDescriptor("d", sp.Medium.DEVICE, "b", [sp.BufferDesc(0, n, dst.data_ptr())]))
+    rng = np.random.default_rng(17)
+    for _ in range(6):
+        b = e.allocate_batch()
+        reqs = []
+        for _ in range(int(rng.integers(1, 12))):
+            ln = int(rng.integers(1, 8 << 20))
+            off = int(rng.integers(0, n - ln))
+            reqs.append(sp.TransferRequest("s", off, "d", off, ln, sp.Direction(int(rng.integers(0, 2)))))
+        e.submit_transfers(b, reqs)
+        st = e.await_batch(b, 30_000_000_000)
+        assert st.state == sp.BatchState.COMPLETE
+        e.free_batch(b)
+    torch.cuda.synchronize()
+    bw, tier, rank = rails_of(topo)
+    ev, dec = replay_live(co, e, sc, res_config(degradation_ratio=1e9), bw, tier, rank)
+    assert len(dec) > 50 and (ev["kind"] == 2).sum() == len(dec)
+    e.stop()
+
+
+# ------------------------------------------------------------------ bytes
+def test_random_transfers_bit_exact():
+    """Acceptance criterion 1 analogue: randomized lengths (1 B .. 32 MiB) and offsets,
+    both directions, HBM->HBM and HBM<->pinned host; delivered bytes memcmp-equal."""
+    topo = fabrics.two_node(3, [2e9, 1e9, 1e9], backend="cuda")
+    e = make_engine(topo, {"resilience": {"degradation_ratio": 1e9}})
+    n = 64 << 20
+    src = dev_buf(n, fill_seed=9)
+    dst = dev_buf(n)
+    hsrc = torch.empty(n, dtype=torch.uint8, pin_memory=True)
+    hsrc.copy_(src.cpu())
+    hdst = torch.zeros(n, dtype=torch.uint8, pin_memory=True)
+    e.register_segment(sp.SegmentDescriptor("s", sp.Medium.DEVICE, "a", [sp.BufferDesc(0, n, src.data_ptr())]))
+    e.register_segment(sp.SegmentDescriptor("d", sp.Medium.DEVICE, "b", [sp.BufferDesc(0, n, dst.data_ptr())]))
+    e.register_segment(sp.SegmentDescriptor("hs", sp.Medium.HOST, "a", [sp.BufferDesc(0, n, hsrc.data_ptr())]))
+    e.register_segment(sp.SegmentDescriptor("hd", sp.Medium.HOST, "b", [sp.BufferDesc(0, n, hdst.data_ptr())]))
+    rng = np.random.default_rng(20260809)
+    for k in range(60):
+        bits = int(rng.integers(0, 26))
+        ln = (1 << bits) | (int(rng.integers(0, 1 << bits)) if bits else 0)
+        ln = min(ln, n)
+        so = int(rng.integers(0, n - ln + 1))
+        do = int(rng.integers(0, n - ln + 1))
+        s_id, d_id = [("s", "d"), ("s", "hd"), ("hs", "d"), ("hs", "hd")][k % 4]
+        b = e.allocate_batch()
+        e.submit_transfer(b, sp.TransferRequest(s_id, so, d_id, do, ln, sp.Direction(k % 2)))
+        st = e.await_batch(b, 30_000_000_000)
+        assert st.state == sp.BatchState.COMPLETE, (k, ln)
+        S = src if s_id == "s" else hsrc
+        D = dst if d_id == "d" else hdst
+        assert torch.equal(S[so:so + ln].cpu(), D[do:do + ln].cpu()), (k, ln, so, do)
+        e.free_batch(b)
+    c = e.counters()
+    assert c["bytes_dispatched"] == c["bytes_terminated"]
+    e.stop()
+
+
+def test_kv_batch_block_table_bit_exact():
+    """Config 3 shape: 4096 x 64 KiB HBM -> pinned host through a random block table,
+    then host -> HBM back into a second pool."""
+    topo = fabrics.kv_offload(DEV, sm_rails=1)
+    e = make_engine(topo, {"resilience": {"degradation_ratio": 1e9}})
+    blk, nb = 64 << 10, 4096
+    pool = dev_buf(blk * nb, fill_seed=7)
+    pool2 = dev_buf(blk * nb)
+    host = torch.zeros(blk * nb, dtype=torch.uint8, pin_memory=True)
+    e.register_segment(sp.SegmentDescriptor("hbm", sp.Medium.DEVICE, f"g{DEV}", [sp.BufferDesc(0, blk * nb, pool.data_ptr())]))
+    e.register_segment(sp.SegmentDescriptor("hbm2", sp.Medium.DEVICE, f"g{DEV}", [sp.BufferDesc(0, blk * nb, pool2.data_ptr())]))
+    e.register_segment(sp.SegmentDescriptor("host", sp.Medium.HOST, f"g{DEV}", [sp.BufferDesc(0, blk * nb, host.data_ptr())]))
+    perm = np.random.default_rng(3).permutation(nb)
+    b = e.allocate_batch()
+    e.submit_transfers(b, [sp.TransferRequest("hbm", i * blk, "host", int(perm[i]) * blk, blk) for i in range(nb)])
+    assert e.await_batch(b, 30_000_000_000).state == sp.BatchState.COMPLETE
+    e.free_batch(b)
+    hv = host.numpy().reshape(nb, blk)
+    assert np.array_equal(hv[perm], pool.cpu().numpy().reshape(nb, blk))
+    p = e.prepare_transfers([sp.TransferRequest("host", int(perm[i]) * blk, "hbm2", i * blk, blk) for i in range(nb)])
+    b = e.allocate_batch()
+    ms = p.run(b)
+    assert ms > 0 and e.batch_status(b).state == sp.BatchState.COMPLETE
+    assert torch.equal(pool, pool2)
+    e.free_batch(b)
+    e.stop()
+
+
+# ------------------------------------------------------------------ batch API semantics
+def test_batch_api_semantics():
+    topo = fabrics.two_node(2, 1e9, backend="cuda")
+    e = make_engine(topo)
+    n = 1 << 20
+    s, d = dev_buf(n, 1), dev_buf(n)
+    e.register_segment(sp.SegmentDescriptor("s", sp.Medium.DEVICE, "a", [sp.BufferDesc(0, n, s.data_ptr())]))
+    e.register_segment(sp.SegmentDescriptor("d", sp.Medium.DEVICE, "b", [sp.BufferDesc(0, n, d.data_ptr())]))
+    b = e.allocate_batch()
+    assert e.batch_status(b).state == sp.BatchState.COMPLETE  # empty batch is complete
+    with pytest.raises(sp.InvalidRangeError):
+        e.submit_transfer(b, sp.TransferRequest("s", n - 10, "d", 0, 20))
+    with pytest.raises(sp.InvalidRangeError):
+        e.submit_transfer(b, sp.TransferRequest("s", 0, "d", 0, 0))
+    with pytest.raises(sp.EngineError, match="unknown segment"):
+        e.submit_transfer(b, sp.TransferRequest("nope", 0, "d", 0, 10))
+    with pytest.raises(sp.EngineError, match="unknown batch"):
+        e.submit_transfer(999999, sp.TransferRequest("s", 0, "d", 0, 10))
+    e.submit_transfer(b, sp.TransferRequest("s", 0, "d", 0, n))
+    assert e.await_batch(b, 10_000_000_000).state == sp.BatchState.COMPLETE
+    with pytest.raises(sp.EngineError, match="already complete"):
+        e.submit_transfer(b, sp.TransferRequest("s", 0, "d", 0, 10))
+    e.free_batch(b)
+    assert torch.equal(s, d)
+    e.stop()
+
+
+# ------------------------------------------------------------------ self-healing
+def test_down_fault_reroutes_with_zero_lost_bytes(co):
+    """Disable one of two rails mid-transfer: its in-flight slices fail (partial prefix
+    writes), three consecutive failures exclude it (resilience.cpp:71-83), retries land
+    on the healthy rail (engine.cpp:405-454); the batch completes bit-exact and the
+    live trace still replays identically."""
+    topo = fabrics.two_node(2, 1e9, backend="cuda")
+    e = make_engine(topo, {"resilience": {"degradation_ratio": 1e9}, "b200": {"chunk_bytes": 65536}})
+    e.trace_enable(1 << 18)
+    n = 256 << 20
+    src, dst = dev_buf(n, 11), dev_buf(n)
+    e.register_segment(sp.SegmentDescriptor("s", sp.Medium.DEVICE, "a", [sp.BufferDesc(0, n, src.data_ptr())]))
+    e.register_segment(sp.SegmentDescriptor("d", sp.Medium.DEVICE, "b", [sp.BufferDesc(0, n, dst.data_ptr())]))
+    # warm the kernel so the engine clock is live, then fail a.r0 from "now" on
+    b0 = e.allocate_batch()
+    e.submit_transfer(b0, sp.TransferRequest("s", 0, "d", 0, 1 << 20))
+    e.await_batch(b0)
+    now = e.now_ns()
+    e.inject_fault("a.r0", sp.FaultEffect.DOWN, now, now + 60_000_000_000)
+    b = e.allocate_batch()
+    for k in range(8):
+        e.submit_transfer(b, sp.TransferRequest("s", k * (n // 8), "d", k * (n // 8), n // 8))
+    st = e.await_batch(b, 60_000_000_000)
+    assert st.state == sp.BatchState.COMPLETE
+    assert torch.equal(src, dst)
+    h = e.heal_stats()
+    assert h["failed_attempts"] >= 3 and h["retried_ok"] > 0
+    assert e.rail_stats(0).health != sp.Health.HEALTHY
+    heal_ms = (h["first_reroute_ok_ns"] - h["fault_start_ns"]) / 1e6
+    assert 0 < heal_ms < 50.0
+    bw, tier, rank = rails_of(topo)
+    replay_live(co, e, sched_config(), res_config(degradation_ratio=1e9), bw, tier, rank)
+    e.stop()
+
+
+def test_all_rails_down_stall_then_complete_after_probing(co):
+    """test_engine.cpp:258-272: every rail down for 100 ms; slices park, the prober
+    (1 s cadence, 2 OK probes) reintegrates the rails, the batch completes bit-exact with
+    zero failed batches; the live trace (with DUE_PROBES / PROBE_DONE) replays identically."""
+    topo = fabrics.two_node(2, 1e9, backend="cuda")
+    e = make_engine(topo, {"resilience": {"degradation_ratio": 1e9}})
+    e.trace_enable(1 << 16)
+    n = 1 << 20
+    src, dst = dev_buf(n, 4), dev_buf(n)
+    e.register_segment(sp.SegmentDescriptor("s", sp.Medium.DEVICE, "a", [sp.BufferDesc(0, n, src.data_ptr())]))
+    e.register_segment(sp.SegmentDescriptor("d", sp.Medium.DEVICE, "b", [sp.BufferDesc(0, n, dst.data_ptr())]))
+    b0 = e.allocate_batch()
+    e.submit_transfer(b0, sp.TransferRequest("s", 0, "d", 0, 4096))
+    e.await_batch(b0)
+    now = e.now_ns()
+    for r in ("a.r0", "a.r1", "b.r0", "b.r1"):
+        e.inject_fault(r, sp.FaultEffect.DOWN, 0, now + 100_000_000)
+    b = e.allocate_batch()
+    e.submit_transfer(b, sp.TransferRequest("s", 0, "d", 0, n))
+    st = e.await_batch(b, 20_000_000_000)
+    assert st.state == sp.BatchState.COMPLETE
+    assert torch.equal(src, dst)
+    assert e.counters()["batches_failed"] == 0
+    assert all(e.rail_stats(r).health == sp.Health.HEALTHY for r in range(4))
+    bw, tier, rank = rails_of(topo)
+    ev, _ = replay_live(co, e, sched_config(), res_config(degradation_ratio=1e9), bw, tier, rank)
+    assert (ev["kind"] == 9).sum() >= 1 and (ev["kind"] == 10).sum() >= 2
+    e.stop()
+
+
+def test_attempts_exhausted_fails_batch_with_all_routes_exhausted():
+    topo = fabrics.two_node(1, 1e9, backend="cuda")
+    e = make_engine(topo, {"resilience": {"degradation_ratio": 1e9, "max_attempts": 1}})
+    n = 4 << 20
+    src, dst = dev_buf(n, 3), dev_buf(n)
+    e.register_segment(sp.SegmentDescriptor("s", sp.Medium.DEVICE, "a", [sp.BufferDesc(0, n, src.data_ptr())]))
+    e.register_segment(sp.SegmentDescriptor("d", sp.Medium.DEVICE, "b", [sp.BufferDesc(0, n, dst.data_ptr())]))
+    e.inject_fault("a.r0", sp.FaultEffect.DOWN, 0, 1 << 62)
+    b = e.allocate_batch()
+    e.submit_transfer(b, sp.TransferRequest("s", 0, "d", 0, n))
+    st = e.await_batch(b, 20_000_000_000)
+    assert st.state == sp.BatchState.FAILED and st.failure_reason == "AllRoutesExhausted"
+    e.free_batch(b)
+    e.stop()
+
+
+# ------------------------------------------------------------------ copy-engine rails
+def test_copy_engine_rail_bit_exact():
+    topo = fabrics.kv_offload(DEV, sm_rails=1, ce_rails=1)
+    e = make_engine(topo, {"resilience": {"degradation_ratio": 1e9}})
+    blk, nb = 1 << 20, 64
+    pool = dev_buf(blk * nb, fill_seed=21)
+    host = torch.zeros(blk * nb, dtype=torch.uint8, pin_memory=True)
+    e.register_segment(sp.SegmentDescriptor("hbm", sp.Medium.DEVICE, f"g{DEV}", [sp.BufferDesc(0, blk * nb, pool.data_ptr())]))
+    e.register_segment(sp.SegmentDescriptor("host", sp.Medium.HOST, f"g{DEV}", [sp.BufferDesc(0, blk * nb, host.data_ptr())]))
+    b = e.allocate_batch()
+    e.submit_transfers(b, [sp.TransferRequest("hbm", i * blk, "host", i * blk, blk) for i in range(nb)])
+    assert e.await_batch(b, 30_000_000_000).state == sp.BatchState.COMPLETE
+    assert torch.equal(pool.cpu(), host)
+    ids = {e.rail_id(r): e.rail_stats(r).bytes_ok for r in range(e.rail_count())}
+    assert ids[f"g{DEV}.ce0"] > 0 and ids[f"g{DEV}.pcie0"] > 0
+    e.stop()
+
+
+# ------------------------------------------------------------------ plugin boundary
+def test_transport_backend_plugin():
+    be = sp.CudaBackend(DEV)
+    be.start()
+    caps = be.capabilities()
+    assert caps.id == b"cuda" and caps.cross_node and caps.same_node
+    n = 8 << 20
+    src, dst = dev_buf(n, 31), dev_buf(n)
+    blob = be.attach_segment_metadata(sp.SegmentDescriptor("s", sp.Medium.DEVICE, "a", [sp.BufferDesc(0, n, src.data_ptr())]))
+    assert blob == b"cuda:s"
+    be.attach_segment_metadata(sp.SegmentDescriptor("d", sp.Medium.DEVICE, "b", [sp.BufferDesc(0, n, dst.data_ptr())]))
+    assert be.attach_segment_metadata(sp.SegmentDescriptor("f", sp.Medium.FILE, "a", [])) is None
+    reqs = [sp.SliceWorkRequest(i, 1, "s", i * 65536, "d", i * 65536, 65536, local_rail=i % 2) for i in range(128)]
+    r = be.post_slices(reqs)
+    assert 0 < r.accepted <= 64 and not r.fatal  # in-flight window: the suffix is backpressure
+    done = []
+    posted = r.accepted
+    import time
+    t0 = time.time()
+    while len(done) < 128 and time.time() - t0 < 30:
+        done += be.poll_completions(32)
+        if posted < 128:
+            posted += be.post_slices(reqs[posted:]).accepted
+    assert sorted(c.slice for c in done) == list(range(128))
+    assert all(c.status == 0 and c.bytes == 65536 for c in done)
+    assert torch.equal(src[:128 * 65536], dst[:128 * 65536])
+    be.latch_fatal()
+    assert be.fatal() and be.post_slices(reqs[:1]).fatal
+    be.stop()
+    be.close()
