@@ -829,6 +829,10 @@ void Engine::debug_words(uint64_t* out, size_t n) {
          static_cast<uint64_t>(cudaStreamQuery(stream_)), ctl_->prof_loops, ctl_->prof_comp_ns,
          ctl_->prof_sub_ns, ctl_->prof_ctl_ns, ctl_->prof_n_comp, ctl_->prof_n_dec};
     for (int q = 0; q < 8; ++q) v.push_back(static_cast<uint64_t>(ctl_->prof_x[q]));
+    v.push_back(static_cast<uint64_t>(ctl_->ce_tail[0]));
+    v.push_back(static_cast<uint64_t>(ctl_->ce_head[0]));
+    v.push_back(static_cast<uint64_t>(ctl_->xc_tail));
+    v.push_back(static_cast<uint64_t>(ctl_->xc_head));
   }
   for (size_t i = 0; i < n; ++i) out[i] = i < v.size() ? v[i] : 0;
 }

@@ -45,7 +45,7 @@ for dst in ("kv/host", "kv/hbm2"):
         st = k.await_batch(b, 5_000_000_000)
         t1 = time.perf_counter()
         d1 = dbg(k)
-        delta = {n: d1[n] - d0[n] for n in ("loops", "comp_ns", "sub_ns", "ctl_ns", "n_comp", "n_dec", "x0", "x1", "x2", "x3")}
+        delta = {n: d1[n] - d0[n] for n in ("comp_ns", "sub_ns", "ctl_ns", "n_comp", "x0", "x1", "x2", "x3", "x4", "x5")}
         print(dst, "ring", it, st.state.name, f"{blk*nb/(t1-t0)/1e9:.2f} GB/s", f"{(t1-t0)*1e3:.2f} ms", delta, flush=True)
         if st.state != sp.BatchState.COMPLETE:
             print(dbg(k))
@@ -57,7 +57,7 @@ for dst in ("kv/host", "kv/hbm2"):
         b = k.allocate_batch()
         ms = p.run(b)
         d1 = dbg(k)
-        delta = {n: d1[n] - d0[n] for n in ("loops", "comp_ns", "sub_ns", "ctl_ns", "n_comp", "n_dec", "x0", "x1", "x2", "x3")}
+        delta = {n: d1[n] - d0[n] for n in ("comp_ns", "sub_ns", "ctl_ns", "n_comp", "x0", "x1", "x2", "x3", "x4", "x5")}
         st = k.batch_status(b)
         print(dst, "prepared", it, st.state.name, f"{blk*nb/(ms*1e-3)/1e9:.2f} GB/s", f"{ms:.3f} ms", delta, flush=True)
         k.free_batch(b)
