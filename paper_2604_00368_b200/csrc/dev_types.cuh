@@ -55,7 +55,7 @@ struct RailState {
 };
 
 // Candidate set (orchestrator.cpp:39-81 output), flattened for the device.
-struct CandSet {
+struct alignas(16) CandSet {
   uint32_t n_locals;
   uint32_t pad_;
   uint32_t local[kMaxLocals];
@@ -186,7 +186,7 @@ struct alignas(64) Control {
   volatile uint64_t error;           // sticky device-side error code (0 = none)
   // scheduler profile (globaltimer ns): loops, time in completions / submissions / control
   volatile uint64_t prof_loops, prof_comp_ns, prof_sub_ns, prof_ctl_ns, prof_n_comp, prof_n_dec;
-  volatile uint64_t prof_x[8];       // fine-grained scheduler phase clocks (SM cycles)
+  volatile uint64_t prof_x[16];      // fine-grained scheduler phase clocks (SM cycles) and counts
 };
 
 // Everything the kernel needs, passed by value.

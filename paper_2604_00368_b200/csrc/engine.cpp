@@ -174,7 +174,7 @@ EngineOptions engine_options_from_json(const std::string& text) {
       eo.work_capacity = static_cast<uint64_t>(b.number_or("work_capacity", double(eo.work_capacity)));
       eo.sub_capacity = static_cast<uint64_t>(b.number_or("sub_capacity", double(eo.sub_capacity)));
       eo.batch_slots = static_cast<uint32_t>(b.number_or("batch_slots", eo.batch_slots));
-      if (eo.block % 32 || eo.block < 64 || eo.block > 1024) throw ConfigError("b200.block must be a multiple of 32 in [64, 1024]");
+      if (eo.block % 32 || eo.block < 192 || eo.block > 1024) throw ConfigError("b200.block must be a multiple of 32 in [192, 1024]");
       if (eo.chunk_bytes < 4096 || (eo.chunk_bytes & (eo.chunk_bytes - 1)) || eo.chunk_bytes > (1ull << 31))
         throw ConfigError("b200.chunk_bytes must be a power of two in [4096, 2^31]");
     }
@@ -201,6 +201,18 @@ Engine::Engine(EngineOptions opts, const std::string& topology_json, int device)
       if (r.ce_index >= 8) throw ConfigError("rail '" + r.id + "': ce_index must be < 8");
     }
   }
+  // Do all SM rails serve pinned host memory (the PCIe staging fabric)?
+  uint32_t n_sm = 0, n_sm_host = 0;
+  for (RailIndex i = 0; i < topo_.rail_count(); ++i) {
+    if (topo_.rail(i).executor != 0) continue;
+    ++n_sm;
+    bool host = false;
+    for (const NodeDecl& n : topo_.nodes())
+      for (const DeviceDecl& d : n.devices)
+        if (d.kind == DeviceKind::kHostMemory && topo_.tier_from_device(d.id, i)) host = true;
+    if (host) ++n_sm_host;
+  }
+  host_only_sm_ = n_sm > 0 && n_sm_host == n_sm;
   slot_busy_.assign(opts_.batch_slots, 0);
 }
 
@@ -440,6 +452,11 @@ void Engine::launch() {
     int sms = 0;
     CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device_));
     grid = sms;
+    // Every SM rail stages through pinned host memory: 48 worker CTAs (384 warps) already
+    // saturate a Gen5 x16 root in each direction, while more writers only deepen the
+    // posted-write backlog that every fence and L2 access then waits behind
+    // (profiles/pcie_peak.json: 1184 writers -> 72 us fences, 21 us L2 reads).
+    if (host_only_sm_) grid = std::min(grid, 1 + kHostLinkCtas);
   }
   ctl_->stop = 0;
   ctl_->drain = drain_ ? 1u : 0u;
@@ -828,7 +845,7 @@ void Engine::debug_words(uint64_t* out, size_t n) {
          ctl_->bytes_terminated, ctl_->failed_attempts, ctl_->retried_ok, ctl_->trace_n,
          static_cast<uint64_t>(cudaStreamQuery(stream_)), ctl_->prof_loops, ctl_->prof_comp_ns,
          ctl_->prof_sub_ns, ctl_->prof_ctl_ns, ctl_->prof_n_comp, ctl_->prof_n_dec};
-    for (int q = 0; q < 8; ++q) v.push_back(static_cast<uint64_t>(ctl_->prof_x[q]));
+    for (int q = 0; q < 16; ++q) v.push_back(static_cast<uint64_t>(ctl_->prof_x[q]));
     v.push_back(static_cast<uint64_t>(ctl_->ce_tail[0]));
     v.push_back(static_cast<uint64_t>(ctl_->ce_head[0]));
     v.push_back(static_cast<uint64_t>(ctl_->xc_tail));

@@ -148,6 +148,8 @@ class Engine {
   std::atomic<bool> ce_run_{false};
   std::vector<cudaStream_t> ce_streams_;
   bool has_ce_ = false;
+  bool host_only_sm_ = false;  // every SM rail stages through pinned host memory
+  static constexpr int kHostLinkCtas = 48;
 };
 
 }  // namespace spray
