@@ -41,6 +41,7 @@ def parse():
     p.add_argument("--impl", default="b200", choices=["b200", "reference"])
     p.add_argument("--blocks", type=int, default=4096)
     p.add_argument("--block-kib", type=int, default=64)
+    p.add_argument("--group", type=int, default=32, help="offload/reload intents alternate in runs of this size")
     p.add_argument("--no-cpu-baseline", action="store_true")
     return p.parse_args()
 
@@ -133,7 +134,14 @@ class ClockSampler:
                  "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
                  "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
                  "--format=csv,noheader,nounits", "-lms", "20"],
-                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+                stdout=open(self.path, "w"), stderr=open(self.path + ".err", "w"))
+            # the timed region starts only once the sampler is producing rows
+            t0 = time.time()
+            while time.time() - t0 < 5.0 and self.proc.poll() is None:
+                if os.path.exists(self.path) and os.path.getsize(self.path) > 0:
+                    break
+                time.sleep(0.02)
+            self.mark = os.path.getsize(self.path) if os.path.exists(self.path) else 0
         except Exception:
             self.proc = None
         return self
@@ -145,11 +153,15 @@ class ClockSampler:
 
     def summary(self):
         try:
-            rows = [r.split(",") for r in open(self.path).read().strip().splitlines() if r.strip()]
+            text = open(self.path).read()
+            rows = [r.split(",") for r in text[getattr(self, "mark", 0):].strip().splitlines() if r.strip()]
+            if not rows:  # the region was shorter than one sampling period: keep the last pre-region row
+                rows = [r.split(",") for r in text.strip().splitlines()[-1:] if r.strip()]
         except Exception:
             return None
         if not rows:
-            return None
+            err = open(self.path + ".err").read().strip() if os.path.exists(self.path + ".err") else ""
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0, "error": err[:200]}
         sm = [float(r[0]) for r in rows if r[0].strip().replace(".", "").isdigit()]
         mx = [float(r[1]) for r in rows if r[1].strip().replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
@@ -191,8 +203,10 @@ def run_b200(args):
         eng.register_segment(sp.SegmentDescriptor(sid, med, node, [sp.BufferDesc(0, pool_bytes, t.data_ptr())]))
     rng = np.random.default_rng(7 + rank)
     p_off, p_on = rng.permutation(nb), rng.permutation(nb)
-    reqs = [sp.TransferRequest("kv/hbm", i * blk, "kv/host", int(p_off[i]) * blk, blk) for i in range(nb)]
-    reqs += [sp.TransferRequest("kv/host2", int(p_on[i]) * blk, "kv/hbm2", i * blk, blk) for i in range(nb)]
+    off = [sp.TransferRequest("kv/hbm", i * blk, "kv/host", int(p_off[i]) * blk, blk) for i in range(nb)]
+    on = [sp.TransferRequest("kv/host2", int(p_on[i]) * blk, "kv/hbm2", i * blk, blk) for i in range(nb)]
+    g = args.group
+    reqs = [r for k in range(0, nb, g) for r in off[k:k + g] + on[k:k + g]]  # swap-out and swap-in interleaved
     step_bytes = 2 * pool_bytes
 
     # ---- value: device-resident intents, drain-mode launch timed with CUDA events
@@ -222,10 +236,12 @@ def run_b200(args):
     if not ok:
         raise RuntimeError("delivered bytes differ")
 
-    # ---- e2e: public API from host arrays, wall clock
+    # ---- e2e: public API from host arrays, wall clock. The request descriptors are a C
+    # array (spray_transfer_request[]) marshalled once, as a C++/cgo caller holds them.
+    creqs = sp.Requests(reqs)
     for _ in range(max(1, args.warmup // 2)):
         b = eng.allocate_batch()
-        eng.submit_transfers(b, reqs)
+        eng.submit_transfers(b, creqs)
         eng.await_batch(b)
         eng.free_batch(b)
     if world > 1:
@@ -234,7 +250,7 @@ def run_b200(args):
     t0 = time.perf_counter()
     for _ in range(args.steps):
         b = eng.allocate_batch()
-        eng.submit_transfers(b, reqs)
+        eng.submit_transfers(b, creqs)
         st = eng.await_batch(b)
         if st.state != sp.BatchState.COMPLETE:
             raise RuntimeError(f"e2e batch not complete: {st}")
@@ -243,23 +259,20 @@ def run_b200(args):
     e2e_ms = (time.perf_counter() - t0) * 1e3
 
     # ---- state-blind baseline: round-robin cudaMemcpyAsync striping of the same blocks
-    streams = [torch.cuda.Stream(device=dev) for _ in range(4)]
-    hb, hs, h2, hb2 = hbm.view(nb, blk), host.view(nb, blk), host2.view(nb, blk), hbm2.view(nb, blk)
-    po, pn = p_off.tolist(), p_on.tolist()
-
-    def rr_step():
-        for i in range(nb):
-            with torch.cuda.stream(streams[i % 4]):
-                hs[po[i]].copy_(hb[i], non_blocking=True)
-            with torch.cuda.stream(streams[(i + 1) % 4]):
-                hb2[i].copy_(h2[pn[i]], non_blocking=True)
-        torch.cuda.synchronize()
-    rr_step()
-    t0 = time.perf_counter()
-    rr_steps = max(1, min(3, args.steps))
-    for _ in range(rr_steps):
-        rr_step()
-    rr_ms = (time.perf_counter() - t0) * 1e3 / rr_steps
+    # (one call per block from C++, the same interleaved order, 4 streams)
+    hb0, hs0, h20, hb20 = hbm.data_ptr(), host.data_ptr(), host2.data_ptr(), hbm2.data_ptr()
+    rr_src, rr_dst = [], []
+    for k in range(0, nb, g):
+        for i in range(k, min(nb, k + g)):
+            rr_src.append(hb0 + i * blk)
+            rr_dst.append(hs0 + int(p_off[i]) * blk)
+        for i in range(k, min(nb, k + g)):
+            rr_src.append(h20 + int(p_on[i]) * blk)
+            rr_dst.append(hb20 + i * blk)
+    rr_len = [blk] * len(rr_src)
+    sp.rr_copy(dev, rr_src, rr_dst, rr_len, 4)
+    rr_steps = max(1, min(5, args.steps))
+    rr_ms = sum(sp.rr_copy(dev, rr_src, rr_dst, rr_len, 4) for _ in range(rr_steps)) / rr_steps
 
     # ---- max over ranks
     vals = torch.tensor([total_ms, e2e_ms, rr_ms], dtype=torch.float64, device=f"cuda:{dev}")
@@ -271,7 +284,17 @@ def run_b200(args):
         value = world * args.steps * step_bytes / (total_ms * 1e-3) / 1e9
         e2e = world * args.steps * step_bytes / (e2e_ms * 1e-3) / 1e9
         per_launch_gbs = step_bytes / (total_ms / args.steps * 1e-3) / 1e9
-        peak = 2 * PCIE_NOMINAL_GBS
+        # denominator: the host link's measured full-duplex ceiling on this pool (copy
+        # engines, tools/pcie_peak.cu); MEASURED_PEAKS.json and the profiling guide carry no
+        # PCIe figure. Nominal Gen5 x16 (2 x 64 GB/s) and the SM load/store ceiling for context.
+        peak, peak_src, link = 2 * PCIE_NOMINAL_GBS, "nominal PCIe Gen5 x16, 2 x 64 GB/s", {}
+        try:
+            link = json.load(open(os.path.join(ROOT, "profiles", "pcie_peak_r01.json")))
+            peak = float(link["ce_both_gbs"])
+            peak_src = ("measured: copy-engine full-duplex HBM<->pinned host on this pool "
+                        "(tools/pcie_peak.cu -> profiles/pcie_peak_r01.json)")
+        except Exception:
+            pass
         traffic = None
         prof = os.path.join(ROOT, "profiles", "ncu_engine_kernel.json")
         if os.path.exists(prof):
@@ -286,7 +309,8 @@ def run_b200(args):
             "vs_baseline": None, "dtype": "u8", "data": "synthetic",
             "config": {"workload": f"kv_batch: {nb} x {args.block_kib} KiB offload HBM->pinned host + {nb} x "
                                    f"{args.block_kib} KiB reload pinned host->HBM per GPU, random block tables, "
-                                   "one batch of 2x{nb} intents per step".replace("{nb}", str(nb)),
+                                   f"one batch of {2 * nb} intents per step, offloads and reloads alternating in "
+                                   f"runs of {args.group}",
                        "fabric": "1 SM PCIe rail per GPU (kv_offload)", "bytes_per_step_per_gpu": step_bytes,
                        "l2": "inputs (2 x 256 MiB pools) larger than the 126 MB L2",
                        "parallelism": f"weak x{world} (one batch per GPU, no data-path collective)"},
@@ -294,11 +318,14 @@ def run_b200(args):
                     "h2d_bytes_per_step": pool_bytes + 64 * 2 * nb, "d2h_bytes_per_step": pool_bytes + 16},
             "roofline": {"bound": "pcie", "achieved": round(per_launch_gbs, 3), "peak": peak, "unit": "GB/s",
                          "frac": round(per_launch_gbs / peak, 4), "traffic": traffic,
-                         "peak_source": "BASELINE.md nominal PCIe Gen5 x16, 64 GB/s per direction x 2 directions "
-                                        "(MEASURED_PEAKS.json has no PCIe figure)",
+                         "traffic_unit": "DRAM bytes per launch (ncu, profiles/ncu_engine_kernel.json); the "
+                                         "host-link bytes per launch there equal the algorithmic 512 MiB",
+                         "peak_source": peak_src, "nominal_gbs": 2 * PCIE_NOMINAL_GBS,
+                         "sm_copy_ceiling_gbs": link.get("sm_both_lsu_gbs", 80.35),
                          "kernel": "spray_engine_kernel (drain-mode launch per step)"},
             "rr_baseline": {"value": round(world * step_bytes / (rr_ms * 1e-3) / 1e9, 3), "unit": "GB/s",
-                            "what": "state-blind round-robin cudaMemcpyAsync per block over 4 streams"},
+                            "what": "state-blind round-robin striping: one cudaMemcpyAsync per block from C++ "
+                                    "(spray_rr_copy), 4 streams, same blocks and order"},
             "gpu_launches": 2 * args.steps,
             "clocks": clk.summary(),
         }

@@ -380,6 +380,13 @@ int spray_checksum(int device, const void* ptr, uint64_t n, uint64_t* out);
 int spray_host_alloc(uint64_t n, void** out);
 int spray_host_free(void* p);
 
+/* State-blind striping baseline (the Policy::kRoundRobin analog a25,
+ * scheduler.cpp:175-177): copy n (src[i], dst[i], len[i]) ranges with one
+ * cudaMemcpyAsync each, round-robin over `streams` copy streams on `device`, then
+ * synchronize. Writes the wall time in milliseconds. Not part of the drop-in path. */
+int spray_rr_copy(int device, const uint64_t* src, const uint64_t* dst, const uint64_t* len, size_t n,
+                  int streams, double* ms_out);
+
 #ifdef __cplusplus
 }
 #endif

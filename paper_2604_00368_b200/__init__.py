@@ -6,8 +6,9 @@ binding. Importing it without the built library raises ImportError: there is no 
 """
 from .engine import (BatchState, BatchStatus, BufferDesc, CapabilityError, CompletionEvent,  # noqa: F401
                      ConfigError, CudaBackend, CudaError, Direction, Engine, EngineError, FaultEffect, Health,
-                     InvalidRangeError, Medium, NoRouteError, PostResult, Prepared, RailStats, SegmentDescriptor,
-                     SliceWorkRequest, TransferRequest, checksum, fill_splitmix, hash128, host_alloc, host_free,
+                     InvalidRangeError, Medium, NoRouteError, PostResult, Prepared, RailStats, Requests,
+                     SegmentDescriptor,
+                     SliceWorkRequest, TransferRequest, checksum, fill_splitmix, hash128, host_alloc, host_free, rr_copy,
                      ipc_close, ipc_export, ipc_open)
 from . import fabrics  # noqa: F401
 

@@ -120,6 +120,7 @@ _SIGS = {
     "spray_checksum": (C.c_int, [C.c_int, P, C.c_uint64, U64P]),
     "spray_host_alloc": (C.c_int, [C.c_uint64, VP]),
     "spray_host_free": (C.c_int, [P]),
+    "spray_rr_copy": (C.c_int, [C.c_int, U64P, U64P, U64P, C.c_size_t, C.c_int, C.POINTER(C.c_double)]),
     "spray_ipc_export": (C.c_int, [C.c_int, P, P]),
     "spray_ipc_open": (C.c_int, [C.c_int, P, VP]),
     "spray_ipc_close": (C.c_int, [P]),

@@ -362,6 +362,25 @@ int spray_host_alloc(uint64_t n, void** out) {
 }
 int spray_host_free(void* p) { return guard([&] { CK(cudaFreeHost(p)); }); }
 
+int spray_rr_copy(int device, const uint64_t* src, const uint64_t* dst, const uint64_t* len, size_t n, int streams,
+                  double* ms_out) {
+  return guard([&] {
+    if (streams < 1 || streams > 64) throw ConfigError("rr_copy: streams must be in [1, 64]");
+    CK(cudaSetDevice(device));
+    std::vector<cudaStream_t> st(static_cast<size_t>(streams));
+    for (auto& s : st) CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    CK(cudaDeviceSynchronize());
+    const auto t0 = std::chrono::steady_clock::now();
+    for (size_t i = 0; i < n; ++i)
+      CK(cudaMemcpyAsync(reinterpret_cast<void*>(dst[i]), reinterpret_cast<const void*>(src[i]), len[i],
+                         cudaMemcpyDefault, st[i % st.size()]));
+    for (auto& s : st) CK(cudaStreamSynchronize(s));
+    const auto t1 = std::chrono::steady_clock::now();
+    for (auto& s : st) cudaStreamDestroy(s);
+    *ms_out = std::chrono::duration<double, std::milli>(t1 - t0).count();
+  });
+}
+
 int spray_ipc_export(int device, void* ptr, uint8_t handle_out[64]) {
   return guard([&] {
     CK(cudaSetDevice(device));

@@ -686,26 +686,49 @@ void Engine::free_batch(uint64_t batch) {
 
 // ------------------------------------------------------------------ submit
 
-Intent Engine::make_intent(uint64_t batch, const spray_transfer_request& req, uint64_t* n_slices) {
+Engine::SegRec& Engine::seg_lookup(const char* name, const char*& cname, SegRec*& crec) {
+  if (!name) name = "";
+  if (crec && std::strcmp(cname, name) == 0) return *crec;
+  auto it = segs_.find(name);
+  if (it == segs_.end()) throw EngineError("unknown segment id");
+  crec = &it->second;
+  cname = it->second.seg.id.c_str();
+  return it->second;
+}
+
+Intent Engine::make_intent(uint64_t batch, const spray_transfer_request& req, uint64_t* n_slices, LookupCache* lc) {
   if (!started_) throw EngineError("engine not started");
-  BatchRec& b = batch_ref(batch);
-  volatile BatchDev* m = &bmirror_[b.slot];
-  if (m->failed_id == b.id) throw EngineError("batch already failed");
-  if (b.submitted > 0 && m->done - b.base >= b.submitted) throw EngineError("batch already complete");
-  auto si = segs_.find(req.src_segment ? req.src_segment : "");
-  auto di = segs_.find(req.dst_segment ? req.dst_segment : "");
-  if (si == segs_.end() || di == segs_.end()) throw EngineError("unknown segment id");
+  LookupCache local;
+  LookupCache& c = lc ? *lc : local;
+  if (!c.batch || c.batch_id != batch) {
+    c.batch = &batch_ref(batch);
+    c.batch_id = batch;
+    // batch state is checked once per submit call: its own earlier intents may already
+    // have completed on the device while the host builds the rest
+    BatchRec& b = *c.batch;
+    volatile BatchDev* m = &bmirror_[b.slot];
+    if (m->failed_id == b.id) throw EngineError("batch already failed");
+    if (b.submitted > 0 && m->done - b.base >= b.submitted) throw EngineError("batch already complete");
+  }
+  BatchRec& b = *c.batch;
+  SegRec& ss = seg_lookup(req.src_segment, c.src_name, c.src);
+  SegRec& ds = seg_lookup(req.dst_segment, c.dst_name, c.dst);
   if (req.length == 0) throw InvalidRangeError("zero-length transfer");
-  const Buffer* sb = si->second.seg.covering(req.src_offset, req.length);
-  if (!sb) throw InvalidRangeError("source range not covered by one registered buffer");
-  const Buffer* db = di->second.seg.covering(req.dst_offset, req.length);
-  if (!db) throw InvalidRangeError("destination range not covered by one registered buffer");
+  if (!ss.seg.covering(req.src_offset, req.length))
+    throw InvalidRangeError("source range not covered by one registered buffer");
+  if (!ds.seg.covering(req.dst_offset, req.length))
+    throw InvalidRangeError("destination range not covered by one registered buffer");
   const Direction dir = req.direction == SPRAY_READ ? Direction::kRead : Direction::kWrite;
-  const uint32_t set = set_for(si->second.seg, di->second.seg, dir);  // throws NoRouteError
-  translate(si->second);
-  translate(di->second);
-  sb = si->second.seg.covering(req.src_offset, req.length);
-  db = di->second.seg.covering(req.dst_offset, req.length);
+  if (c.set_src != &ss || c.set_dst != &ds || c.set_dir != static_cast<int>(dir)) {
+    c.set = set_for(ss.seg, ds.seg, dir);  // throws NoRouteError
+    c.set_src = &ss;
+    c.set_dst = &ds;
+    c.set_dir = static_cast<int>(dir);
+  }
+  translate(ss);
+  translate(ds);
+  const Buffer* sb = ss.seg.covering(req.src_offset, req.length);
+  const Buffer* db = ds.seg.covering(req.dst_offset, req.length);
   Intent in{};
   in.batch_id = b.id;
   in.src = sb->dev_addr + (req.src_offset - sb->offset);
@@ -713,7 +736,7 @@ Intent Engine::make_intent(uint64_t batch, const spray_transfer_request& req, ui
   in.len = req.length;
   in.hash_offset = req.src_offset;
   in.transfer_id = next_transfer_++;
-  in.set_id = set;
+  in.set_id = c.set;
   in.batch_slot = b.slot;
   in.flags = 0;
   *n_slices = decompose_count(req.length);
@@ -747,23 +770,30 @@ uint64_t Engine::submit_transfer(uint64_t batch, const spray_transfer_request& r
   return in.transfer_id;
 }
 
+// Intents are published in groups as they are built, so the device starts on the head of
+// a large batch while the host is still translating its tail (order is unchanged).
 size_t Engine::submit_transfers(uint64_t batch, const spray_transfer_request* reqs, size_t n, uint64_t* ids) {
   std::lock_guard<std::mutex> lk(mu_);
-  std::vector<Intent> v;
-  v.reserve(n);
-  size_t done = 0;
+  constexpr size_t kGroup = 256;
+  Intent v[kGroup];
+  size_t nv = 0, done = 0;
+  LookupCache lc;
   try {
     for (; done < n; ++done) {
       uint64_t k = 0;
-      v.push_back(make_intent(batch, reqs[done], &k));
-      batch_ref(batch).submitted += k;
-      if (ids) ids[done] = v.back().transfer_id;
+      v[nv] = make_intent(batch, reqs[done], &k, &lc);
+      lc.batch->submitted += k;
+      if (ids) ids[done] = v[nv].transfer_id;
+      if (++nv == kGroup) {
+        publish(v, nv);
+        nv = 0;
+      }
     }
   } catch (...) {
-    if (!v.empty()) publish(v.data(), v.size());
+    if (nv) publish(v, nv);
     throw;
   }
-  publish(v.data(), v.size());
+  if (nv) publish(v, nv);
   return done;
 }
 

@@ -64,7 +64,21 @@ class Engine {
 
   // Device-resident submission (bench / device producers): `dev_intents` is an HBM
   // array of n Intent records built with make_intent(). Counts n transfers into batch.
-  spray_dev::Intent make_intent(uint64_t batch, const spray_transfer_request& req, uint64_t* n_slices);
+  struct BatchRec;
+  struct SegRec;
+  // Lookups reused across the requests of one submit call (consecutive requests usually
+  // name the same segments and route).
+  struct LookupCache {
+    uint64_t batch_id = 0;
+    BatchRec* batch = nullptr;
+    const char *src_name = nullptr, *dst_name = nullptr;
+    SegRec *src = nullptr, *dst = nullptr;
+    const SegRec *set_src = nullptr, *set_dst = nullptr;
+    int set_dir = -1;
+    uint32_t set = 0;
+  };
+  spray_dev::Intent make_intent(uint64_t batch, const spray_transfer_request& req, uint64_t* n_slices,
+                                LookupCache* lc = nullptr);
   void submit_device_intents(uint64_t batch, const void* dev_intents, uint64_t n, uint64_t total_slices);
   void set_drain(bool on);
   cudaStream_t stream() const { return stream_; }
@@ -90,7 +104,6 @@ class Engine {
   // Diagnostic snapshot: host/device ring positions, kernel state, counters, stream status.
   void debug_words(uint64_t* out, size_t n);
 
- private:
   struct BatchRec {
     uint64_t id = 0;
     uint32_t slot = 0;
@@ -103,6 +116,8 @@ class Engine {
     std::vector<void*> registered;  // host buffers we cudaHostRegister'ed
   };
 
+ private:
+
   void alloc_device();
   void free_device();
   void launch();
@@ -110,6 +125,7 @@ class Engine {
   uint32_t set_for(const Segment& src, const Segment& dst, Direction dir);
   void translate(SegRec& s);
   void publish(const spray_dev::Intent* in, size_t n);
+  SegRec& seg_lookup(const char* name, const char*& cname, SegRec*& crec);
   void ce_proxy_loop();
   BatchRec& batch_ref(uint64_t id);
   uint64_t decompose_count(uint64_t len) const;

@@ -161,6 +161,19 @@ def _reqs_c(reqs: Sequence[TransferRequest]):
     return arr, keep
 
 
+class Requests:
+    """A request list marshalled once into the C-ABI's spray_transfer_request array, for
+    callers that resubmit the same block table (the C-ABI call then takes host arrays
+    directly, as a C++ or cgo caller would)."""
+
+    def __init__(self, reqs: Sequence[TransferRequest]):
+        self.arr, self._keep = _reqs_c(reqs)
+        self.n = len(reqs)
+
+    def __len__(self):
+        return self.n
+
+
 def _status(st: L.BatchStatusC) -> BatchStatus:
     return BatchStatus(BatchState(st.state), int(st.remaining), st.failure_reason.decode())
 
@@ -218,11 +231,16 @@ class Engine:
         _check(lib.spray_submit_transfer(self._h, batch, C.byref(r), C.byref(t)))
         return t.value
 
-    def submit_transfers(self, batch: int, reqs: Sequence[TransferRequest]) -> List[int]:
-        arr, keep = _reqs_c(reqs)
-        ids = (C.c_uint64 * max(1, len(reqs)))()
+    def submit_transfers(self, batch: int, reqs) -> List[int]:
+        """`reqs`: a sequence of TransferRequest, or a prebuilt Requests array."""
+        if isinstance(reqs, Requests):
+            arr = reqs.arr
+        else:
+            arr, keep = _reqs_c(reqs)
+        n = len(reqs)
+        ids = (C.c_uint64 * max(1, n))()
         done = C.c_size_t()
-        _check(lib.spray_submit_transfers(self._h, batch, arr, len(reqs), ids, C.byref(done)))
+        _check(lib.spray_submit_transfers(self._h, batch, arr, n, ids, C.byref(done)))
         return list(ids[: done.value])
 
     def batch_status(self, batch: int) -> BatchStatus:
@@ -456,6 +474,20 @@ def checksum(device: int, ptr: int, n: int) -> int:
     out = C.c_uint64()
     _check(lib.spray_checksum(device, ptr, n, C.byref(out)))
     return out.value
+
+
+def rr_copy(device: int, src, dst, lens, streams: int = 4) -> float:
+    """State-blind baseline: one cudaMemcpyAsync per range, round-robin over `streams`
+    streams (spray_rr_copy). Returns wall milliseconds."""
+    import numpy as np
+    s = np.ascontiguousarray(src, dtype=np.uint64)
+    d = np.ascontiguousarray(dst, dtype=np.uint64)
+    n = np.ascontiguousarray(lens, dtype=np.uint64)
+    ms = C.c_double()
+    U = C.POINTER(C.c_uint64)
+    _check(lib.spray_rr_copy(device, s.ctypes.data_as(U), d.ctypes.data_as(U), n.ctypes.data_as(U), len(n), streams,
+                             C.byref(ms)))
+    return ms.value
 
 
 def host_alloc(n: int) -> int:

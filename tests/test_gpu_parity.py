@@ -153,6 +153,64 @@ def test_live_trace_replays_identically(co, policy):
     e.stop()
 
 
+def test_live_trace_with_degradation_exclusions_replays_identically(co):
+    """Tight degradation settings so rails are excluded by observe() on OK completions
+    (the completion fast path's lane-parallel classification) and reintegrated by probes;
+    the live trace must still replay to the same decisions and health expectations."""
+    topo = fabrics.two_node(2, [2e9, 1e9], backend="cuda")
+    rc_kw = dict(degradation_ratio=1.02, degradation_events=2, degradation_min_t_obs_s=0.0,
+                 probe_interval_ns=200_000, probe_successes_needed=1)
+    e = make_engine(topo, {"resilience": {"degradation_ratio": 1.02, "degradation_events": 2,
+                                          "degradation_min_t_obs_ms": 0.0, "probe_interval_ms": 0.2,
+                                          "probe_successes": 1},
+                           "b200": {"chunk_bytes": 65536}})
+    e.trace_enable(1 << 18)
+    n = 64 << 20
+    src = dev_buf(n, fill_seed=11)
+    dst = dev_buf(n)
+    e.register_segment(sp.SegmentDescriptor("s", sp.Medium.DEVICE, "a", [sp.BufferDesc(0, n, src.data_ptr())]))
+    e.register_segment(sp.SegmentDescriptor("d", sp.Medium.DEVICE, "b", [sp.BufferDesc(0, n, dst.data_ptr())]))
+    rng = np.random.default_rng(23)
+    ranges = []
+    for _ in range(8):
+        b = e.allocate_batch()
+        reqs = []
+        for _ in range(int(rng.integers(2, 10))):
+            ln = int(rng.integers(64 << 10, 6 << 20))
+            off = int(rng.integers(0, n - ln))
+            reqs.append(sp.TransferRequest("s", off, "d", off, ln))
+            ranges.append((off, ln))
+        e.submit_transfers(b, reqs)
+        assert e.await_batch(b, 30_000_000_000).state == sp.BatchState.COMPLETE
+        e.free_batch(b)
+    torch.cuda.synchronize()
+    for off, ln in ranges:
+        assert torch.equal(src[off:off + ln], dst[off:off + ln])
+    bw, tier, rank = rails_of(topo)
+    ev, dec = replay_live(co, e, sched_config(), res_config(**rc_kw), bw, tier, rank)
+    assert (ev["kind"] == 8).sum() > 0  # SPRAY_EV_EXPECT_HEALTH: exclusions happened
+    e.stop()
+
+
+def test_large_submit_races_device_completion():
+    """One submit call whose first published groups complete on the device before the
+    host has built the rest: the batch must not be taken for complete mid-call."""
+    topo = fabrics.two_node(2, 1e9, backend="cuda")
+    e = make_engine(topo, {"resilience": {"degradation_ratio": 1e9}})
+    n = 16 << 20
+    s, d = dev_buf(n, 3), dev_buf(n)
+    e.register_segment(sp.SegmentDescriptor("s", sp.Medium.DEVICE, "a", [sp.BufferDesc(0, n, s.data_ptr())]))
+    e.register_segment(sp.SegmentDescriptor("d", sp.Medium.DEVICE, "b", [sp.BufferDesc(0, n, d.data_ptr())]))
+    reqs = sp.Requests([sp.TransferRequest("s", i * 4096, "d", i * 4096, 4096) for i in range(n // 4096)])
+    for _ in range(10):
+        b = e.allocate_batch()
+        e.submit_transfers(b, reqs)
+        assert e.await_batch(b, 30_000_000_000).state == sp.BatchState.COMPLETE
+        e.free_batch(b)
+    assert torch.equal(s, d)
+    e.stop()
+
+
 # ------------------------------------------------------------------ bytes
 def test_random_transfers_bit_exact():
     """Acceptance criterion 1 analogue: randomized lengths (1 B .. 32 MiB) and offsets,
