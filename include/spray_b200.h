@@ -311,7 +311,7 @@ int spray_trace_fetch(spray_engine* e, spray_trace_event* events, size_t cap, si
 int spray_trace_candidates(spray_engine* e, int32_t* stream, size_t cap, size_t* len);
 
 /* ------------------------------------------------------------------ backend (plugin) */
-/* spray::SliceWorkRequest (backend.hpp:15-27) as a 64-byte POD: segment ids become
+/* spray::SliceWorkRequest (backend.hpp:15-27) as an 88-byte POD: segment ids become
  * their Hash128 (common.hpp:111-120), as on the reference TCP wire. */
 typedef struct spray_slice_wr {  /* 88 bytes */
   uint64_t slice;
