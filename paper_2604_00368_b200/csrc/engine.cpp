@@ -3,6 +3,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <deque>
 #include <cstring>
 #include <immintrin.h>
 
@@ -201,8 +202,14 @@ Engine::Engine(EngineOptions opts, const std::string& topology_json, int device)
       if (r.ce_index >= 8) throw ConfigError("rail '" + r.id + "': ce_index must be < 8");
     }
   }
-  // Do all SM rails serve pinned host memory (the PCIe staging fabric)?
-  uint32_t n_sm = 0, n_sm_host = 0;
+  // A single-GPU host-staging fabric: one node with device memory (no peer HBM paths)
+  // and every SM rail serving pinned host memory.
+  uint32_t n_sm = 0, n_sm_host = 0, n_dev_nodes = 0;
+  for (const NodeDecl& n : topo_.nodes()) {
+    bool dev = false;
+    for (const DeviceDecl& d : n.devices) dev = dev || d.kind == DeviceKind::kDeviceMemory;
+    n_dev_nodes += dev ? 1 : 0;
+  }
   for (RailIndex i = 0; i < topo_.rail_count(); ++i) {
     if (topo_.rail(i).executor != 0) continue;
     ++n_sm;
@@ -212,7 +219,7 @@ Engine::Engine(EngineOptions opts, const std::string& topology_json, int device)
         if (d.kind == DeviceKind::kHostMemory && topo_.tier_from_device(d.id, i)) host = true;
     if (host) ++n_sm_host;
   }
-  host_only_sm_ = n_sm > 0 && n_sm_host == n_sm;
+  host_only_sm_ = n_dev_nodes == 1 && n_sm > 0 && n_sm_host == n_sm;
   slot_busy_.assign(opts_.batch_slots, 0);
 }
 
@@ -944,14 +951,17 @@ std::vector<int32_t> Engine::trace_candidates() {
 // Copy-engine rails: the device publishes CeOrders into a mapped ring; this thread
 // issues one cudaMemcpyAsync per order on the rail's side stream, and posts the
 // completion into the mapped external-completion ring the device scheduler drains.
+// CE rails: the device publishes copy orders per CE stream; this thread issues them with
+// cudaMemcpyAsync in order, records one event per group of orders taken in a pass, and
+// completes a group when its event fires (a stream's copies finish in issue order, so
+// only the oldest group of each stream is ever queried).
 void Engine::ce_proxy_loop() {
   cudaSetDevice(device_);
-  struct Pending {
+  struct Group {
     cudaEvent_t ev;
-    CeOrder o;
-    bool failed;
+    std::vector<CeOrder> orders;
   };
-  std::vector<Pending> pend;
+  std::deque<Group> fifo[8];
   std::vector<cudaEvent_t> pool;
   uint64_t head[8] = {0};
   uint64_t xc_tail = ctl_->xc_tail;
@@ -965,17 +975,19 @@ void Engine::ce_proxy_loop() {
     std::atomic_thread_fence(std::memory_order_release);
     ctl_->xc_tail = ++xc_tail;
   };
+  constexpr int kMaxGroup = 32;
   while (ce_run_.load()) {
     bool any = false;
     for (int k = 0; k < 8; ++k) {
-      while (head[k] < ctl_->ce_tail[k]) {
+      Group g;
+      g.ev = nullptr;
+      while (head[k] < ctl_->ce_tail[k] && g.orders.size() < size_t(kMaxGroup)) {
         volatile CeOrder* vo = &ce_ring_[k * E_.ce_cap + (head[k] % E_.ce_cap)];
         if (vo->stamp != head[k] + 1) break;
         CeOrder o;
         o.src = vo->src; o.dst = vo->dst; o.len = vo->len; o.slice = vo->slice; o.attempt = vo->attempt;
         o.rail = vo->rail; o.ce_index = vo->ce_index; o.stamp = vo->stamp;
         ++head[k];
-        ctl_->ce_head[k] = head[k];
         any = true;
         const volatile FaultDev* f = &faults_[o.rail];
         const uint64_t now = ctl_->device_now;
@@ -983,34 +995,37 @@ void Engine::ce_proxy_loop() {
           post(o, kStFailed);
           continue;
         }
-        cudaEvent_t ev;
-        if (pool.empty()) {
-          cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
-        } else {
-          ev = pool.back();
-          pool.pop_back();
-        }
         cudaMemcpyAsync(reinterpret_cast<void*>(o.dst), reinterpret_cast<const void*>(o.src), o.len, cudaMemcpyDefault,
                         ce_streams_[k]);
-        cudaEventRecord(ev, ce_streams_[k]);
-        pend.push_back(Pending{ev, o, false});
+        g.orders.push_back(o);
+      }
+      ctl_->ce_head[k] = head[k];
+      if (!g.orders.empty()) {
+        if (pool.empty()) {
+          cudaEventCreateWithFlags(&g.ev, cudaEventDisableTiming);
+        } else {
+          g.ev = pool.back();
+          pool.pop_back();
+        }
+        cudaEventRecord(g.ev, ce_streams_[k]);
+        fifo[k].push_back(std::move(g));
       }
     }
-    for (size_t i = 0; i < pend.size();) {
-      const cudaError_t q = cudaEventQuery(pend[i].ev);
-      if (q == cudaErrorNotReady) {
-        ++i;
-        continue;
+    for (int k = 0; k < 8; ++k) {
+      while (!fifo[k].empty()) {
+        Group& g = fifo[k].front();
+        const cudaError_t q = cudaEventQuery(g.ev);
+        if (q == cudaErrorNotReady) break;
+        for (const CeOrder& o : g.orders) post(o, q == cudaSuccess ? kStOk : kStFailed);
+        pool.push_back(g.ev);
+        fifo[k].pop_front();
+        any = true;
       }
-      post(pend[i].o, q == cudaSuccess ? kStOk : kStFailed);
-      pool.push_back(pend[i].ev);
-      pend[i] = pend.back();
-      pend.pop_back();
-      any = true;
     }
     if (!any) std::this_thread::sleep_for(std::chrono::microseconds(5));
   }
-  for (auto& p : pend) cudaEventSynchronize(p.ev), pool.push_back(p.ev);
+  for (int k = 0; k < 8; ++k)
+    for (auto& g : fifo[k]) cudaEventSynchronize(g.ev), pool.push_back(g.ev);
   for (auto e : pool) cudaEventDestroy(e);
 }
 

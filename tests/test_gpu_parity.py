@@ -338,6 +338,32 @@ def test_down_fault_reroutes_with_zero_lost_bytes(co):
     e.stop()
 
 
+@pytest.mark.parametrize("delay_us", [0, 150, 600])
+def test_fault_starting_mid_transfer_is_bit_exact(delay_us):
+    """A DOWN fault that begins while chunks of the rail are in flight (the scheduled-
+    fault path: 16 KiB steps, stop at the fault's start, partial prefix write): every
+    affected attempt must be reported FAILED and re-sprayed; no holes in delivered bytes."""
+    topo = fabrics.two_node(2, 1e9, backend="cuda")
+    e = make_engine(topo, {"resilience": {"degradation_ratio": 1e9}})
+    n = 512 << 20
+    src, dst = dev_buf(n, 13 + delay_us), dev_buf(n)
+    e.register_segment(sp.SegmentDescriptor("s", sp.Medium.DEVICE, "a", [sp.BufferDesc(0, n, src.data_ptr())]))
+    e.register_segment(sp.SegmentDescriptor("d", sp.Medium.DEVICE, "b", [sp.BufferDesc(0, n, dst.data_ptr())]))
+    b0 = e.allocate_batch()
+    e.submit_transfer(b0, sp.TransferRequest("s", 0, "d", 0, 1 << 20))
+    e.await_batch(b0)
+    b = e.allocate_batch()
+    e.submit_transfers(b, [sp.TransferRequest("s", k * (n // 16), "d", k * (n // 16), n // 16) for k in range(16)])
+    now = e.now_ns()
+    e.inject_fault("a.r0", sp.FaultEffect.DOWN, now + delay_us * 1000, now + 60_000_000_000)
+    st = e.await_batch(b, 60_000_000_000)
+    assert st.state == sp.BatchState.COMPLETE
+    assert torch.equal(src, dst)
+    c = e.counters()
+    assert c["bytes_dispatched"] == c["bytes_terminated"]
+    e.stop()
+
+
 def test_all_rails_down_stall_then_complete_after_probing(co):
     """test_engine.cpp:258-272: every rail down for 100 ms; slices park, the prober
     (1 s cadence, 2 OK probes) reintegrates the rails, the batch completes bit-exact with
