@@ -177,6 +177,20 @@ int spray_engine_debug(spray_engine* e, uint64_t* out, size_t n);
 int spray_heal_stats(spray_engine* e, uint64_t* fault_start_ns, uint64_t* first_reroute_ok_ns,
                      uint64_t* failed_attempts, uint64_t* retried_ok);
 
+/* Dataflow gates: how a GPU re-emits slices it received (relay paths, broadcast chains;
+ * the exchange step of SURVEY.md §8(e)). `flags` is one uint32 counter per chunk_bytes
+ * granule of the (single-buffer) segment, in device memory reachable from this GPU and
+ * shared by the producing and the consuming engine (zero-initialised by the caller).
+ *   PRODUCE (2): a slice this engine writes into the segment advances the counters of
+ *                its granules when it completes OK (after a system fence).
+ *   CONSUME (1): this engine's copies out of the segment wait, granule by granule,
+ *                until the producer has delivered it (gate_timeout_ms, then the attempt
+ *                fails and is retried). Offsets and slice sizes on a gated segment must
+ *                be multiples of chunk_bytes. SM rails only. Register while idle. */
+enum { SPRAY_GATE_CONSUME = 1, SPRAY_GATE_PRODUCE = 2 };
+int spray_gate_segment(spray_engine* e, const char* segment_id, int role, void* flags);
+int spray_engine_chunk_bytes(spray_engine* e, uint64_t* out);
+
 /* Device-resident submission (intents built once, kept in HBM, reused by many batches).
  * prepare: validates and plans every request exactly like submit_transfer and stages the
  * resulting intents in HBM. run: submits them all into `batch` as one bulk record and

@@ -105,6 +105,8 @@ _SIGS = {
     "spray_clear_faults": (C.c_int, [P]),
     "spray_engine_now_ns": (C.c_uint64, [P]),
     "spray_heal_stats": (C.c_int, [P, U64P, U64P, U64P, U64P]),
+    "spray_gate_segment": (C.c_int, [P, C.c_char_p, C.c_int, P]),
+    "spray_engine_chunk_bytes": (C.c_int, [P, U64P]),
     "spray_engine_debug": (C.c_int, [P, U64P, C.c_size_t]),
     "spray_trace_enable": (C.c_int, [P, C.c_size_t]),
     "spray_trace_fetch": (C.c_int, [P, P, C.c_size_t, SZP, P, C.c_size_t, SZP]),

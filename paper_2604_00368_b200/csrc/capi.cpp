@@ -151,6 +151,14 @@ int spray_heal_stats(spray_engine* e, uint64_t* fs, uint64_t* ok, uint64_t* fa, 
   return guard([&] { e->eng->heal_stats(fs, ok, fa, ro); });
 }
 
+int spray_gate_segment(spray_engine* e, const char* segment_id, int role, void* flags) {
+  return guard([&] { e->eng->gate_segment(segment_id ? segment_id : "", static_cast<uint32_t>(role), flags); });
+}
+
+int spray_engine_chunk_bytes(spray_engine* e, uint64_t* out) {
+  return guard([&] { *out = e->eng->chunk_bytes(); });
+}
+
 int spray_engine_debug(spray_engine* e, uint64_t* out, size_t n) {
   return guard([&] { e->eng->debug_words(out, n); });
 }

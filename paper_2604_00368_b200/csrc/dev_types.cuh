@@ -189,6 +189,22 @@ struct alignas(64) Control {
   volatile uint64_t prof_x[16];      // fine-grained scheduler phase clocks (SM cycles) and counts
 };
 
+// Dataflow gate on one segment (forwarding, relays, broadcast chains; SURVEY.md §8(e):
+// GPU k re-emits slices it received). Per granule (= chunk_bytes) of [lo, hi):
+//   CONSUME: this engine's workers read a granule only once flags[g] > consumed[g];
+//            consumed[g] (this engine's HBM) advances when a slice reading it completes OK.
+//   PRODUCE: when a slice writing the granule completes OK, flags[g] (any GPU) advances,
+//            after a system fence (PUBLISH warp).
+enum : uint32_t { kGateConsume = 1, kGateProduce = 2 };
+constexpr int kMaxGates = 4;
+struct GateDev {
+  uint64_t lo, hi;         // device-usable address range of the segment
+  uint32_t* flags;         // per-granule counters (written by the producing engine)
+  uint32_t* consumed;      // per-granule consumption counters (CONSUME only, local HBM)
+  uint32_t role;
+  uint32_t pad_;
+};
+
 // Everything the kernel needs, passed by value.
 struct EngineDev {
   Control* ctl;                      // mapped host
@@ -232,8 +248,10 @@ struct EngineDev {
   uint64_t scratch;                            // HBM probe scratch (2 x probe_bytes)
   uint64_t chunk_bytes;                        // SM work granule (power of two)
   uint32_t chunk_shift;                        // log2(chunk_bytes)
-  uint32_t pad_cs_;
+  uint32_t n_gates;                            // dataflow gates (0: none, the common case)
   uint64_t epoch;                              // globaltimer at engine time 0
+  uint64_t gate_timeout_ns;                    // a consumer gives up on a granule after this
+  GateDev gates[kMaxGates];
 };
 
 // scalars persisted in EngineDev::persist between launches

@@ -165,8 +165,10 @@ EngineOptions engine_options_from_json(const std::string& text) {
     if (j.contains("b200")) {
       const Json& b = j.at("b200");
       reject_unknown(b, {"grid", "block", "chunk_bytes", "idle_exit_ms", "slice_capacity", "work_capacity",
-                         "sub_capacity", "batch_slots"},
+                         "sub_capacity", "batch_slots", "gate_timeout_ms"},
                      "b200");
+      if (b.contains("gate_timeout_ms"))
+        eo.gate_timeout_ns = static_cast<uint64_t>(b.at("gate_timeout_ms").as_number() * 1e6);
       eo.grid = static_cast<int>(b.number_or("grid", eo.grid));
       eo.block = static_cast<int>(b.number_or("block", eo.block));
       eo.chunk_bytes = static_cast<uint64_t>(b.number_or("chunk_bytes", double(eo.chunk_bytes)));
@@ -385,6 +387,8 @@ void Engine::alloc_device() {
   E_.probe_backoff_cap = opts_.res.probe_backoff_cap;
   E_.scratch = reinterpret_cast<uint64_t>(dev(2 * E_.probe_bytes));
   E_.chunk_bytes = opts_.chunk_bytes;
+  E_.gate_timeout_ns = opts_.gate_timeout_ns;
+  E_.n_gates = 0;
   E_.chunk_shift = 0;
   while ((1ull << E_.chunk_shift) < opts_.chunk_bytes) ++E_.chunk_shift;
   // engine epoch on the device clock
@@ -619,6 +623,52 @@ uint64_t Engine::decompose_count(uint64_t len) const {  // scheduler.cpp:94-106
   return (len + size - 1) / size;
 }
 
+// ------------------------------------------------------------------ dataflow gates
+
+void Engine::gate_segment(const std::string& seg_id, uint32_t role, void* flags) {
+  std::lock_guard<std::mutex> lk(mu_);
+  if (!started_) throw EngineError("engine not started");
+  if (role != kGateConsume && role != kGateProduce) throw ConfigError("gate role must be consume (1) or produce (2)");
+  if (!flags) throw ConfigError("gate: flags array is null");
+  if (has_ce_) throw ConfigError("dataflow gates are served by SM rails only (the fabric has copy-engine rails)");
+  if (E_.n_gates >= uint32_t(kMaxGates)) throw ConfigError("too many gated segments (max 4)");
+  auto it = segs_.find(seg_id);
+  if (it == segs_.end()) throw EngineError("unknown segment id");
+  SegRec& s = it->second;
+  if (s.seg.buffers.size() != 1) throw ConfigError("gate: the segment must have exactly one buffer");
+  translate(s);
+  for (const auto& kv : batches_) {
+    volatile BatchDev* m = &bmirror_[kv.second.slot];
+    if (m->failed_id != kv.second.id && m->done - kv.second.base < kv.second.submitted)
+      throw EngineError("gate: register gates while no batch is in flight");
+  }
+  // the running kernel holds the previous EngineDev: let it exit, the next launch has the gate
+  if (ctl_->state != 0) {
+    ctl_->stop = 1;
+    std::atomic_thread_fence(std::memory_order_seq_cst);
+    CK(cudaStreamSynchronize(stream_));
+    ctl_->stop = 0;
+    ctl_->state = 0;
+  }
+  const Buffer& bf = s.seg.buffers.front();
+  const uint64_t granules = (bf.length + opts_.chunk_bytes - 1) / opts_.chunk_bytes;
+  GateDev g{};
+  g.lo = bf.dev_addr;
+  g.hi = bf.dev_addr + bf.length;
+  g.flags = static_cast<uint32_t*>(flags);
+  g.role = role;
+  if (role == kGateConsume) {
+    CK(cudaSetDevice(device_));
+    void* p = nullptr;
+    CK(cudaMalloc(&p, granules * sizeof(uint32_t)));
+    CK(cudaMemset(p, 0, granules * sizeof(uint32_t)));
+    dev_allocs_.push_back(p);
+    g.consumed = static_cast<uint32_t*>(p);
+  }
+  E_.gates[E_.n_gates++] = g;
+  s.gated = true;
+}
+
 // ------------------------------------------------------------------ batches
 
 Engine::BatchRec& Engine::batch_ref(uint64_t id) {
@@ -726,6 +776,15 @@ Intent Engine::make_intent(uint64_t batch, const spray_transfer_request& req, ui
   if (!ds.seg.covering(req.dst_offset, req.length))
     throw InvalidRangeError("destination range not covered by one registered buffer");
   const Direction dir = req.direction == SPRAY_READ ? Direction::kRead : Direction::kWrite;
+  if (ss.gated || ds.gated) {  // gated segments: every chunk is exactly one granule
+    const uint64_t cb = opts_.chunk_bytes;
+    uint64_t nsl = req.length / opts_.sched.min_slice_size;
+    if (nsl == 0) nsl = 1;
+    if (nsl > opts_.sched.max_slices_per_transfer) nsl = opts_.sched.max_slices_per_transfer;
+    const uint64_t size = (req.length + nsl - 1) / nsl;
+    if (req.src_offset % cb || req.dst_offset % cb || (nsl > 1 && size % cb))
+      throw InvalidRangeError("gated segment: offsets and slice sizes must be multiples of b200.chunk_bytes");
+  }
   if (c.set_src != &ss || c.set_dst != &ds || c.set_dir != static_cast<int>(dir)) {
     c.set = set_for(ss.seg, ds.seg, dir);  // throws NoRouteError
     c.set_src = &ss;

@@ -40,6 +40,7 @@ struct EngineOptions {
   uint64_t sub_capacity = 1ull << 16;
   uint32_t batch_slots = 1u << 16;
   uint32_t max_sets = 1024;
+  uint64_t gate_timeout_ns = 10'000'000'000ull;  // dataflow gate wait before an attempt fails
 };
 
 // engine_options_from_json (engine.cpp:1199-1307): unknown keys rejected.
@@ -101,6 +102,11 @@ class Engine {
                                        std::string* backend);
 
   int device() const { return device_; }
+  uint64_t chunk_bytes() const { return opts_.chunk_bytes; }
+  // Dataflow gate on a registered single-buffer segment (role kGateConsume/kGateProduce);
+  // `flags` = one uint32 counter per chunk_bytes granule, device memory reachable from this
+  // GPU (the producer's and the consumer's engines share it).
+  void gate_segment(const std::string& seg_id, uint32_t role, void* flags);
   // Diagnostic snapshot: host/device ring positions, kernel state, counters, stream status.
   void debug_words(uint64_t* out, size_t n);
 
@@ -113,6 +119,7 @@ class Engine {
   struct SegRec {
     Segment seg;
     bool translated = false;
+    bool gated = false;             // a dataflow gate covers this segment
     std::vector<void*> registered;  // host buffers we cudaHostRegister'ed
   };
 

@@ -294,6 +294,19 @@ class Engine:
     def now_ns(self) -> int:
         return int(lib.spray_engine_now_ns(self._h))
 
+    # ---- dataflow gates (forwarding / relays / broadcast chains)
+    GATE_CONSUME, GATE_PRODUCE = 1, 2
+
+    def gate_segment(self, segment_id: str, role: int, flags_ptr: int):
+        """Gate a registered single-buffer segment: `flags_ptr` points at one zeroed uint32
+        counter per chunk_bytes() granule, shared by the producing and consuming engines."""
+        _check(lib.spray_gate_segment(self._h, segment_id.encode(), int(role), flags_ptr))
+
+    def chunk_bytes(self) -> int:
+        v = C.c_uint64()
+        _check(lib.spray_engine_chunk_bytes(self._h, C.byref(v)))
+        return v.value
+
     def heal_stats(self):
         a, b, c, d = (C.c_uint64() for _ in range(4))
         _check(lib.spray_heal_stats(self._h, C.byref(a), C.byref(b), C.byref(c), C.byref(d)))

@@ -364,6 +364,45 @@ def test_fault_starting_mid_transfer_is_bit_exact(delay_us):
     e.stop()
 
 
+def test_dataflow_gate_forwarding_chain_bit_exact():
+    """Two engines form a 2-hop relay on one GPU: engine A copies src -> mid and produces
+    mid's granules; engine B copies mid -> dst and consumes them granule by granule while
+    A is still writing. Repeated runs reuse the same counters; bytes stay exact."""
+    topo = fabrics.two_node(1, 1e9, backend="cuda")
+    cfg = {"resilience": {"degradation_ratio": 1e9},
+           "b200": {"grid": 64, "gate_timeout_ms": 20000, "chunk_bytes": 65536}}  # 64 KiB slices = granules
+    a, b = make_engine(topo, cfg), make_engine(topo, cfg)
+    n = 64 << 20
+    src, mid, dst = dev_buf(n, 41), dev_buf(n), dev_buf(n)
+    for e in (a, b):
+        e.register_segment(sp.SegmentDescriptor("src", sp.Medium.DEVICE, "a", [sp.BufferDesc(0, n, src.data_ptr())]))
+        e.register_segment(sp.SegmentDescriptor("mid", sp.Medium.DEVICE, "b", [sp.BufferDesc(0, n, mid.data_ptr())]))
+        e.register_segment(sp.SegmentDescriptor("dst", sp.Medium.DEVICE, "b", [sp.BufferDesc(0, n, dst.data_ptr())]))
+    cb = a.chunk_bytes()
+    flags = torch.zeros(n // cb, dtype=torch.int32, device=f"cuda:{DEV}")
+    a.gate_segment("mid", sp.Engine.GATE_PRODUCE, flags.data_ptr())
+    b.gate_segment("mid", sp.Engine.GATE_CONSUME, flags.data_ptr())
+    with pytest.raises(sp.InvalidRangeError):
+        bx = b.allocate_batch()
+        b.submit_transfer(bx, sp.TransferRequest("mid", 100, "dst", 0, cb))
+    for run in range(3):
+        mid.zero_()
+        dst.zero_()
+        torch.cuda.synchronize()
+        bb = b.allocate_batch()
+        b.submit_transfer(bb, sp.TransferRequest("mid", 0, "dst", 0, n))  # waits on the gate
+        ba = a.allocate_batch()
+        a.submit_transfer(ba, sp.TransferRequest("src", 0, "mid", 0, n))
+        assert a.await_batch(ba, 60_000_000_000).state == sp.BatchState.COMPLETE
+        assert b.await_batch(bb, 60_000_000_000).state == sp.BatchState.COMPLETE
+        a.free_batch(ba)
+        b.free_batch(bb)
+        assert torch.equal(src, dst), run
+        assert int(flags.min()) == run + 1 and int(flags.max()) == run + 1
+    a.stop()
+    b.stop()
+
+
 def test_all_rails_down_stall_then_complete_after_probing(co):
     """test_engine.cpp:258-272: every rail down for 100 ms; slices park, the prober
     (1 s cadence, 2 OK probes) reintegrates the rails, the batch completes bit-exact with

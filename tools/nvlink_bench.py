@@ -105,6 +105,25 @@ def c2(args):
             evs[1].synchronize()
             times.append(evs[0].elapsed_time(evs[1]))
     out["memcpy_peer_gbs"] = round(n / (min(times) * 1e-3) / 1e9, 2)
+    # raw SM peer stores without any scheduling: the plugin backend's group copy kernel
+    # (one launch, 64 x 16 MiB slices, 128 KiB chunks over 4 CTAs per SM)
+    be = sp.CudaBackend(0)
+    be.start()
+    be.attach_segment_metadata(sp.SegmentDescriptor("s", sp.Medium.DEVICE, "g0", [sp.BufferDesc(0, n, src.data_ptr())]))
+    be.attach_segment_metadata(sp.SegmentDescriptor("d", sp.Medium.DEVICE, "g1", [sp.BufferDesc(0, n, dst.data_ptr())]))
+    k = 64
+    reqs = [sp.SliceWorkRequest(i, 1, "s", i * (n // k), "d", i * (n // k), n // k) for i in range(k)]
+    best_raw = 1e9
+    for _ in range(args.reps + 1):
+        torch.cuda.synchronize(0)
+        t0 = time.perf_counter()
+        assert be.post_slices(reqs).accepted == k
+        got = 0
+        while got < k:
+            got += len(be.poll_completions(k))
+        best_raw = min(best_raw, time.perf_counter() - t0)
+    be.stop()
+    out["raw_sm_peer_gbs"] = round(n / best_raw / 1e9, 2)
     return out
 
 
@@ -167,6 +186,64 @@ def c4(args):
             "ms": round(best, 3), "delivered_gbs": round((g - 1) * n / (best * 1e-3) / 1e9, 2)}
 
 
+def c4chain(args):
+    """Pipelined relay chain GPU0 -> GPU1 -> ... -> GPU(g-1): engine k forwards granule i of
+    its copy as soon as it has arrived (dataflow gates), so every receiver's ingress is
+    busy at once instead of GPU0's egress carrying g-1 copies."""
+    import threading
+    g = torch.cuda.device_count()
+    n = args.size
+    ws = [buf(0, n, 5)] + [buf(j, n) for j in range(1, g)]
+    engines, preps = [], []
+    flags = {}
+    for k in range(g - 1):
+        e = engine(k, list(range(g)), args.sm_rails, 0)
+        cb = e.chunk_bytes()
+        reg(e, f"w{k}", k, ws[k])
+        reg(e, f"w{k + 1}", k + 1, ws[k + 1])
+        if k + 1 not in flags:
+            flags[k + 1] = torch.zeros((n + cb - 1) // cb, dtype=torch.int32, device=f"cuda:{k + 1}")
+        e.gate_segment(f"w{k + 1}", sp.Engine.GATE_PRODUCE, flags[k + 1].data_ptr())
+        if k > 0:
+            e.gate_segment(f"w{k}", sp.Engine.GATE_CONSUME, flags[k].data_ptr())
+        engines.append(e)
+        preps.append(e.prepare_transfers([sp.TransferRequest(f"w{k}", 0, f"w{k + 1}", 0, n)]))
+    walls, kms = [], []
+    for rep in range(args.reps + 1):
+        for t in ws[1:]:
+            t.zero_()
+        for d in range(g):
+            torch.cuda.synchronize(d)
+        batches = [e.allocate_batch() for e in engines]
+        res = [None] * len(engines)
+
+        def run(k):
+            res[k] = preps[k].run(batches[k])
+        th = [threading.Thread(target=run, args=(k,)) for k in range(len(engines))]
+        t0 = time.perf_counter()
+        for t in th:
+            t.start()
+        for t in th:
+            t.join()
+        wall = time.perf_counter() - t0
+        for e, b in zip(engines, batches):
+            assert e.batch_status(b).state == sp.BatchState.COMPLETE
+            e.free_batch(b)
+        if rep:
+            walls.append(wall)
+            kms.append(max(res))
+    ref = sp.checksum(0, ws[0].data_ptr(), n)
+    for j in range(1, g):
+        assert sp.checksum(j, ws[j].data_ptr(), n) == ref, j
+    for e in engines:
+        e.stop()
+    best = min(kms)
+    return {"mode": "c4-chain", "gpus": g, "bytes": n, "delivered": (g - 1) * n, "slowest_engine_ms": round(best, 3),
+            "wall_ms": round(min(walls) * 1e3, 3),
+            "delivered_gbs": round((g - 1) * n / (best * 1e-3) / 1e9, 2),
+            "per_receiver_gbs": round(n / (best * 1e-3) / 1e9, 2)}
+
+
 def c5(args):
     n = args.size
     src, dst = buf(0, n, 91), buf(1, n)
@@ -225,14 +302,14 @@ def c5(args):
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("mode", choices=["c2", "elephant", "c4", "c5"])
+    ap.add_argument("mode", choices=["c2", "elephant", "c4", "c4chain", "c5"])
     ap.add_argument("--size", type=int, default=GiB)
     ap.add_argument("--sm-rails", type=int, default=1)
     ap.add_argument("--ce-rails", type=int, default=0)
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--fault-after-ms", type=float, default=0.3)
     args = ap.parse_args()
-    out = {"c2": c2, "elephant": elephant, "c4": c4, "c5": c5}[args.mode](args)
+    out = {"c2": c2, "elephant": elephant, "c4": c4, "c4chain": c4chain, "c5": c5}[args.mode](args)
     print(json.dumps(out), flush=True)
     os._exit(0)
 
