@@ -189,6 +189,7 @@ int spray_plan_candidates(spray_engine* e, const char* src, const char* dst, int
 // ------------------------------------------------------------------ prepared (device-resident) batches
 int spray_prepare_transfers(spray_engine* e, const spray_transfer_request* reqs, size_t n, spray_prepared** out) {
   return guard([&] {
+    CK(cudaSetDevice(e->eng->device()));  // callers may be on any thread / current device
     // plan + validate through a scratch batch, exactly like submit_transfer
     const uint64_t b = e->eng->allocate_batch();
     std::vector<Intent> v(n);
@@ -219,6 +220,7 @@ int spray_run_prepared(spray_engine* e, uint64_t batch, spray_prepared* p, float
   return guard([&] {
     if (p->owner != e) throw EngineError("prepared set belongs to another engine");
     Engine& g = *e->eng;
+    CK(cudaSetDevice(g.device()));  // events below belong to the engine's device
     g.set_drain(true);
     // make sure no launch is resident, so this one is bracketed alone
     while (g.running_kernel()) std::this_thread::sleep_for(std::chrono::microseconds(50));

@@ -575,6 +575,7 @@ uint32_t Engine::set_for(const Segment& src, const Segment& dst, Direction dir) 
   const std::string key = src.id + '\x1f' + dst.id + '\x1f' + (dir == Direction::kWrite ? 'w' : 'r');
   auto it = set_cache_.find(key);
   if (it != set_cache_.end()) return it->second;
+  CK(cudaSetDevice(device_));
   auto routes = build_plan(topo_, src, dst, dir, opts_.sched.penalty, caps_);  // throws NoRouteError
   const Route& r = routes.front();
   if (r.candidates.size() > size_t(kMaxLocals)) throw ConfigError("route has more than 32 local rails");
@@ -960,6 +961,7 @@ void Engine::heal_stats(uint64_t* fs, uint64_t* ok, uint64_t* fa, uint64_t* ro) 
 // ------------------------------------------------------------------ trace
 
 void Engine::trace_enable(size_t cap) {
+  CK(cudaSetDevice(device_));
   std::lock_guard<std::mutex> lk(mu_);
   if (!started_) throw EngineError("engine not started");
   ctl_->stop = 1;
@@ -983,6 +985,7 @@ void Engine::trace_enable(size_t cap) {
 }
 
 void Engine::trace_fetch(spray_trace_event* ev, size_t cap, size_t* n, spray_decision* dec, size_t dcap, size_t* nd) {
+  CK(cudaSetDevice(device_));
   std::lock_guard<std::mutex> lk(mu_);
   if (!started_ || !trace_cap_) throw EngineError("tracing not enabled");
   // quiesce the kernel so the trace is complete and stable
