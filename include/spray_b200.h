@@ -191,6 +191,13 @@ enum { SPRAY_GATE_CONSUME = 1, SPRAY_GATE_PRODUCE = 2 };
 int spray_gate_segment(spray_engine* e, const char* segment_id, int role, void* flags);
 int spray_engine_chunk_bytes(spray_engine* e, uint64_t* out);
 
+/* TelemetrySnapshot::to_csv (telemetry.cpp:123-158): one row per (window, rail),
+ * columns window_start_ms,rail_id,bytes_ok,bytes_failed,queue_depth_bytes,p50_us,p99_us,
+ * health_state,throughput_gbps, from the device's per-rail window cells (the last 1024
+ * windows of stats_window_ms, default 10 ms). Writes at most cap-1 bytes + NUL; *len gets
+ * the full length. */
+int spray_telemetry_csv(spray_engine* e, char* buf, size_t cap, size_t* len);
+
 /* Device-resident submission (intents built once, kept in HBM, reused by many batches).
  * prepare: validates and plans every request exactly like submit_transfer and stages the
  * resulting intents in HBM. run: submits them all into `batch` as one bulk record and

@@ -107,6 +107,7 @@ _SIGS = {
     "spray_heal_stats": (C.c_int, [P, U64P, U64P, U64P, U64P]),
     "spray_gate_segment": (C.c_int, [P, C.c_char_p, C.c_int, P]),
     "spray_engine_chunk_bytes": (C.c_int, [P, U64P]),
+    "spray_telemetry_csv": (C.c_int, [P, C.c_char_p, C.c_size_t, SZP]),
     "spray_engine_debug": (C.c_int, [P, U64P, C.c_size_t]),
     "spray_trace_enable": (C.c_int, [P, C.c_size_t]),
     "spray_trace_fetch": (C.c_int, [P, P, C.c_size_t, SZP, P, C.c_size_t, SZP]),

@@ -155,6 +155,18 @@ int spray_gate_segment(spray_engine* e, const char* segment_id, int role, void* 
   return guard([&] { e->eng->gate_segment(segment_id ? segment_id : "", static_cast<uint32_t>(role), flags); });
 }
 
+int spray_telemetry_csv(spray_engine* e, char* buf, size_t cap, size_t* len) {
+  return guard([&] {
+    const std::string s = e->eng->telemetry_csv();
+    if (len) *len = s.size();
+    if (buf && cap) {
+      const size_t n = std::min(cap - 1, s.size());
+      std::memcpy(buf, s.data(), n);
+      buf[n] = 0;
+    }
+  });
+}
+
 int spray_engine_chunk_bytes(spray_engine* e, uint64_t* out) {
   return guard([&] { *out = e->eng->chunk_bytes(); });
 }

@@ -189,6 +189,17 @@ struct alignas(64) Control {
   volatile uint64_t prof_x[16];      // fine-grained scheduler phase clocks (SM cycles) and counts
 };
 
+// Telemetry window cell (telemetry.hpp:37-44 WindowCell), one per rail per window in an
+// HBM ring of kTeleWindows windows: the STATE warp updates it at every completion.
+constexpr uint32_t kTeleWindows = 1024;
+struct TeleCell {
+  uint64_t window;          // absolute window index (engine ns / window_ns); ~0 = empty
+  uint64_t bytes_ok, bytes_failed;
+  int64_t queue_close;
+  uint32_t health_close, touched;
+  uint32_t hist[48];        // OK service times, LatencyHistogram buckets
+};
+
 // Dataflow gate on one segment (forwarding, relays, broadcast chains; SURVEY.md §8(e):
 // GPU k re-emits slices it received). Per granule (= chunk_bytes) of [lo, hi):
 //   CONSUME: this engine's workers read a granule only once flags[g] > consumed[g];
@@ -252,6 +263,8 @@ struct EngineDev {
   uint64_t epoch;                              // globaltimer at engine time 0
   uint64_t gate_timeout_ns;                    // a consumer gives up on a granule after this
   GateDev gates[kMaxGates];
+  TeleCell* tele;                              // HBM [n_rails][kTeleWindows] telemetry windows
+  uint64_t window_ns;                          // telemetry window (stats_window_ms, default 10 ms)
 };
 
 // scalars persisted in EngineDev::persist between launches

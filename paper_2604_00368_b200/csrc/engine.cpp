@@ -3,6 +3,8 @@
 
 #include <algorithm>
 #include <chrono>
+#include <cmath>
+#include <cstdio>
 #include <deque>
 #include <cstring>
 #include <immintrin.h>
@@ -107,6 +109,11 @@ EngineOptions engine_options_from_json(const std::string& text) {
                        "staging", "burst", "ring_capacity", "stats", "stats_window_ms", "seed", "sim", "memory",
                        "instance_id", "b200"},
                    "root");
+    if (j.contains("stats_window_ms")) {  // Telemetry window (engine.cpp:1186-1197 key set)
+      const double ms = j.at("stats_window_ms").as_number();
+      if (!(ms >= 0.001)) throw ConfigError("stats_window_ms must be >= 0.001");
+      eo.window_ns = static_cast<uint64_t>(ms * 1e6);
+    }
     if (j.contains("backends")) {
       eo.backends.clear();
       for (const Json& b : j.at("backends").arr) eo.backends.push_back(b.as_string());
@@ -345,6 +352,12 @@ void Engine::alloc_device() {
   E_.slot_fail = static_cast<uint32_t*>(dev(sizeof(uint32_t) * opts_.slice_capacity));
   E_.faults_hbm = static_cast<FaultDev*>(dev(sizeof(FaultDev) * kMaxRails));
   E_.next_free = static_cast<unsigned long long*>(dev(sizeof(unsigned long long) * kMaxRails));
+  {  // telemetry windows: every cell starts empty (window = ~0)
+    const size_t tb = sizeof(TeleCell) * kTeleWindows * std::max<size_t>(1, topo_.rail_count());
+    E_.tele = static_cast<TeleCell*>(dev(tb));
+    CK(cudaMemset(E_.tele, 0xff, tb));
+    E_.window_ns = opts_.window_ns;
+  }
   E_.exit_flag = static_cast<uint32_t*>(dev(sizeof(uint32_t)));
   E_.has_ce = has_ce_ ? 1u : 0u;
   E_.work_cap = opts_.work_capacity;
@@ -435,7 +448,12 @@ void Engine::start() {
   started_ = true;
   if (has_ce_) {
     ce_run_ = true;
-    ce_thread_ = std::thread([this] { ce_proxy_loop(); });
+    xc_reserve_ = ctl_->xc_head;
+    uint32_t used = 0;  // one proxy thread per CE stream a rail uses: cudaMemcpyAsync calls in parallel
+    for (RailIndex i = 0; i < topo_.rail_count(); ++i)
+      if (topo_.rail(i).executor == 1) used |= 1u << (topo_.rail(i).ce_index & 7);
+    for (int k = 0; k < 8; ++k)
+      if (used & (1u << k)) ce_threads_.emplace_back([this, k] { ce_proxy_loop(k); });
   }
 }
 
@@ -449,7 +467,9 @@ void Engine::stop() {
   ctl_->state = 0;
   if (has_ce_) {
     ce_run_ = false;
-    if (ce_thread_.joinable()) ce_thread_.join();
+    for (auto& t : ce_threads_)
+      if (t.joinable()) t.join();
+    ce_threads_.clear();
   }
   started_ = false;
 }
@@ -622,6 +642,71 @@ uint64_t Engine::decompose_count(uint64_t len) const {  // scheduler.cpp:94-106
   if (n > opts_.sched.max_slices_per_transfer) n = opts_.sched.max_slices_per_transfer;
   const uint64_t size = (len + n - 1) / n;
   return (len + size - 1) / size;
+}
+
+// ------------------------------------------------------------------ telemetry export
+
+// LatencyHistogram::percentile_us (telemetry.cpp:28-44)
+static double percentile_us(const uint32_t* h, double q) {
+  uint64_t n = 0;
+  for (int b = 0; b < 48; ++b) n += h[b];
+  if (n == 0) return 0.0;
+  uint64_t rank = static_cast<uint64_t>(std::ceil(q * static_cast<double>(n)));
+  if (rank == 0) rank = 1;
+  uint64_t seen = 0;
+  for (int b = 0; b < 48; ++b) {
+    seen += h[b];
+    if (seen >= rank) return std::exp2((static_cast<double>(b) + 0.5) / 2.0);
+  }
+  return std::exp2(48.0 / 2.0);
+}
+
+static const char* health_name(uint32_t h) {  // health_state_name (scheduler.cpp)
+  return h == kHealthy ? "healthy" : h == kExcluded ? "excluded" : "probing";
+}
+
+// TelemetrySnapshot::to_csv (telemetry.cpp:123-158) from the device window cells: the same
+// columns, one row per (window, rail) over the windows the ring still holds, health and
+// queue carried forward through untouched windows.
+std::string Engine::telemetry_csv() {
+  std::string out =
+      "window_start_ms,rail_id,bytes_ok,bytes_failed,queue_depth_bytes,p50_us,p99_us,health_state,throughput_gbps\n";
+  if (!started_) return out;
+  CK(cudaSetDevice(device_));
+  const size_t nr = topo_.rail_count();
+  std::vector<TeleCell> cells(nr * kTeleWindows);
+  CK(cudaMemcpyAsync(cells.data(), E_.tele, cells.size() * sizeof(TeleCell), cudaMemcpyDeviceToHost, copy_stream_));
+  CK(cudaStreamSynchronize(copy_stream_));
+  uint64_t last = 0;
+  bool any = false;
+  for (const TeleCell& c : cells)
+    if (c.window != ~0ull && c.touched) last = std::max(last, c.window), any = true;
+  if (!any) return out;
+  const uint64_t first = last >= kTeleWindows - 1 ? last - (kTeleWindows - 1) : 0;
+  const double window_s = static_cast<double>(opts_.window_ns) * 1e-9;
+  char line[320];
+  std::vector<uint32_t> health(nr, kHealthy);
+  std::vector<int64_t> queue(nr, 0);
+  for (uint64_t w = first; w <= last; ++w) {
+    for (size_t r = 0; r < nr; ++r) {
+      const TeleCell& c = cells[r * kTeleWindows + (w % kTeleWindows)];
+      const bool hit = c.window == w && c.touched;
+      if (hit) {
+        health[r] = c.health_close;
+        queue[r] = c.queue_close;
+      }
+      static const uint32_t kZero[48] = {};
+      const uint32_t* h = hit ? c.hist : kZero;
+      const uint64_t ok = hit ? c.bytes_ok : 0, failed = hit ? c.bytes_failed : 0;
+      std::snprintf(line, sizeof(line), "%llu,%s,%llu,%llu,%lld,%.3f,%.3f,%s,%.6f\n",
+                    static_cast<unsigned long long>(w * (opts_.window_ns / 1000000ull)), topo_.rail(r).id.c_str(),
+                    static_cast<unsigned long long>(ok), static_cast<unsigned long long>(failed),
+                    static_cast<long long>(queue[r]), percentile_us(h, 0.50), percentile_us(h, 0.99),
+                    health_name(health[r]), static_cast<double>(ok) * 8.0 / window_s / 1e9);
+      out += line;
+    }
+  }
+  return out;
 }
 
 // ------------------------------------------------------------------ dataflow gates
@@ -1013,81 +1098,78 @@ std::vector<int32_t> Engine::trace_candidates() {
 // Copy-engine rails: the device publishes CeOrders into a mapped ring; this thread
 // issues one cudaMemcpyAsync per order on the rail's side stream, and posts the
 // completion into the mapped external-completion ring the device scheduler drains.
-// CE rails: the device publishes copy orders per CE stream; this thread issues them with
-// cudaMemcpyAsync in order, records one event per group of orders taken in a pass, and
-// completes a group when its event fires (a stream's copies finish in issue order, so
-// only the oldest group of each stream is ever queried).
-void Engine::ce_proxy_loop() {
+// CE rails: the device publishes copy orders per CE stream; one thread per stream issues
+// them with cudaMemcpyAsync in order, records one event per group of orders taken in a
+// pass, and completes a group when its event fires (a stream's copies finish in issue
+// order, so only the oldest group is ever queried). Completions go to the shared
+// completion ring: a slot is reserved atomically, and its stamp (written last) publishes
+// it to the device (HOSTRX reads the stamped prefix).
+void Engine::ce_proxy_loop(int k) {
   cudaSetDevice(device_);
   struct Group {
     cudaEvent_t ev;
     std::vector<CeOrder> orders;
   };
-  std::deque<Group> fifo[8];
+  std::deque<Group> fifo;
   std::vector<cudaEvent_t> pool;
-  uint64_t head[8] = {0};
-  uint64_t xc_tail = ctl_->xc_tail;
+  uint64_t head = ctl_->ce_head[k];
   auto post = [&](const CeOrder& o, uint32_t status) {
-    while (xc_tail - ctl_->xc_head >= E_.xc_cap) _mm_pause();
-    volatile Completion* c = &xc_ring_[xc_tail % E_.xc_cap];
+    const uint64_t pos = xc_reserve_.fetch_add(1);
+    while (pos - ctl_->xc_head >= E_.xc_cap) _mm_pause();
+    volatile Completion* c = &xc_ring_[pos % E_.xc_cap];
     c->slice = o.slice;
     c->attempt = o.attempt;
     c->status = status;
     c->rail = o.rail;
     std::atomic_thread_fence(std::memory_order_release);
-    ctl_->xc_tail = ++xc_tail;
+    c->stamp = static_cast<uint32_t>(pos + 1);
   };
   constexpr int kMaxGroup = 32;
   while (ce_run_.load()) {
     bool any = false;
-    for (int k = 0; k < 8; ++k) {
-      Group g;
-      g.ev = nullptr;
-      while (head[k] < ctl_->ce_tail[k] && g.orders.size() < size_t(kMaxGroup)) {
-        volatile CeOrder* vo = &ce_ring_[k * E_.ce_cap + (head[k] % E_.ce_cap)];
-        if (vo->stamp != head[k] + 1) break;
-        CeOrder o;
-        o.src = vo->src; o.dst = vo->dst; o.len = vo->len; o.slice = vo->slice; o.attempt = vo->attempt;
-        o.rail = vo->rail; o.ce_index = vo->ce_index; o.stamp = vo->stamp;
-        ++head[k];
-        any = true;
-        const volatile FaultDev* f = &faults_[o.rail];
-        const uint64_t now = ctl_->device_now;
-        if (f->active && f->effect == 0 && f->start <= now && now < f->end) {
-          post(o, kStFailed);
-          continue;
-        }
-        cudaMemcpyAsync(reinterpret_cast<void*>(o.dst), reinterpret_cast<const void*>(o.src), o.len, cudaMemcpyDefault,
-                        ce_streams_[k]);
-        g.orders.push_back(o);
+    Group g;
+    g.ev = nullptr;
+    while (head < ctl_->ce_tail[k] && g.orders.size() < size_t(kMaxGroup)) {
+      volatile CeOrder* vo = &ce_ring_[k * E_.ce_cap + (head % E_.ce_cap)];
+      if (vo->stamp != head + 1) break;
+      CeOrder o;
+      o.src = vo->src; o.dst = vo->dst; o.len = vo->len; o.slice = vo->slice; o.attempt = vo->attempt;
+      o.rail = vo->rail; o.ce_index = vo->ce_index; o.stamp = vo->stamp;
+      ++head;
+      any = true;
+      const volatile FaultDev* f = &faults_[o.rail];
+      const uint64_t now = ctl_->device_now;
+      if (f->active && f->effect == 0 && f->start <= now && now < f->end) {
+        post(o, kStFailed);
+        continue;
       }
-      ctl_->ce_head[k] = head[k];
-      if (!g.orders.empty()) {
-        if (pool.empty()) {
-          cudaEventCreateWithFlags(&g.ev, cudaEventDisableTiming);
-        } else {
-          g.ev = pool.back();
-          pool.pop_back();
-        }
-        cudaEventRecord(g.ev, ce_streams_[k]);
-        fifo[k].push_back(std::move(g));
-      }
+      cudaMemcpyAsync(reinterpret_cast<void*>(o.dst), reinterpret_cast<const void*>(o.src), o.len, cudaMemcpyDefault,
+                      ce_streams_[k]);
+      g.orders.push_back(o);
     }
-    for (int k = 0; k < 8; ++k) {
-      while (!fifo[k].empty()) {
-        Group& g = fifo[k].front();
-        const cudaError_t q = cudaEventQuery(g.ev);
-        if (q == cudaErrorNotReady) break;
-        for (const CeOrder& o : g.orders) post(o, q == cudaSuccess ? kStOk : kStFailed);
-        pool.push_back(g.ev);
-        fifo[k].pop_front();
-        any = true;
+    ctl_->ce_head[k] = head;
+    if (!g.orders.empty()) {
+      if (pool.empty()) {
+        cudaEventCreateWithFlags(&g.ev, cudaEventDisableTiming);
+      } else {
+        g.ev = pool.back();
+        pool.pop_back();
       }
+      cudaEventRecord(g.ev, ce_streams_[k]);
+      fifo.push_back(std::move(g));
+    }
+    while (!fifo.empty()) {
+      Group& h = fifo.front();
+      const cudaError_t q = cudaEventQuery(h.ev);
+      if (q == cudaErrorNotReady) break;
+      for (const CeOrder& o : h.orders) post(o, q == cudaSuccess ? kStOk : kStFailed);
+      pool.push_back(h.ev);
+      fifo.pop_front();
+      any = true;
     }
     if (!any) std::this_thread::sleep_for(std::chrono::microseconds(5));
   }
-  for (int k = 0; k < 8; ++k)
-    for (auto& g : fifo[k]) cudaEventSynchronize(g.ev), pool.push_back(g.ev);
+  for (auto& h : fifo) cudaEventSynchronize(h.ev), pool.push_back(h.ev);
   for (auto e : pool) cudaEventDestroy(e);
 }
 

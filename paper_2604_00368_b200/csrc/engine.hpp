@@ -41,6 +41,7 @@ struct EngineOptions {
   uint32_t batch_slots = 1u << 16;
   uint32_t max_sets = 1024;
   uint64_t gate_timeout_ns = 10'000'000'000ull;  // dataflow gate wait before an attempt fails
+  uint64_t window_ns = 10'000'000;              // telemetry window (stats_window_ms)
 };
 
 // engine_options_from_json (engine.cpp:1199-1307): unknown keys rejected.
@@ -107,6 +108,8 @@ class Engine {
   // `flags` = one uint32 counter per chunk_bytes granule, device memory reachable from this
   // GPU (the producer's and the consumer's engines share it).
   void gate_segment(const std::string& seg_id, uint32_t role, void* flags);
+  // TelemetrySnapshot::to_csv columns from the device's per-rail window cells.
+  std::string telemetry_csv();
   // Diagnostic snapshot: host/device ring positions, kernel state, counters, stream status.
   void debug_words(uint64_t* out, size_t n);
 
@@ -133,7 +136,7 @@ class Engine {
   void translate(SegRec& s);
   void publish(const spray_dev::Intent* in, size_t n);
   SegRec& seg_lookup(const char* name, const char*& cname, SegRec*& crec);
-  void ce_proxy_loop();
+  void ce_proxy_loop(int k);
   BatchRec& batch_ref(uint64_t id);
   uint64_t decompose_count(uint64_t len) const;
 
@@ -167,8 +170,9 @@ class Engine {
   bool drain_ = false;
 
   // CE proxy
-  std::thread ce_thread_;
+  std::vector<std::thread> ce_threads_;
   std::atomic<bool> ce_run_{false};
+  std::atomic<uint64_t> xc_reserve_{0};  // next CE completion ring position (proxy threads)
   std::vector<cudaStream_t> ce_streams_;
   bool has_ce_ = false;
   bool host_only_sm_ = false;  // every SM rail stages through pinned host memory

@@ -302,6 +302,14 @@ class Engine:
         counter per chunk_bytes() granule, shared by the producing and consuming engines."""
         _check(lib.spray_gate_segment(self._h, segment_id.encode(), int(role), flags_ptr))
 
+    def telemetry_csv(self) -> str:
+        """TelemetrySnapshot::to_csv columns from the device telemetry windows."""
+        n = C.c_size_t()
+        _check(lib.spray_telemetry_csv(self._h, None, 0, C.byref(n)))
+        buf = C.create_string_buffer(n.value + 1)
+        _check(lib.spray_telemetry_csv(self._h, buf, n.value + 1, C.byref(n)))
+        return buf.value.decode()
+
     def chunk_bytes(self) -> int:
         v = C.c_uint64()
         _check(lib.spray_engine_chunk_bytes(self._h, C.byref(v)))

@@ -403,6 +403,36 @@ def test_dataflow_gate_forwarding_chain_bit_exact():
     b.stop()
 
 
+def test_telemetry_csv_windows_account_every_byte():
+    """TelemetrySnapshot::to_csv columns (telemetry.cpp:123-158) from the device window
+    cells: per-window bytes sum to the delivered bytes, per rail; percentiles ordered."""
+    topo = fabrics.two_node(2, [2e9, 1e9], backend="cuda")
+    e = make_engine(topo, {"stats_window_ms": 1, "resilience": {"degradation_ratio": 1e9}})
+    n = 96 << 20
+    src, dst = dev_buf(n, 3), dev_buf(n)
+    e.register_segment(sp.SegmentDescriptor("s", sp.Medium.DEVICE, "a", [sp.BufferDesc(0, n, src.data_ptr())]))
+    e.register_segment(sp.SegmentDescriptor("d", sp.Medium.DEVICE, "b", [sp.BufferDesc(0, n, dst.data_ptr())]))
+    for k in range(4):
+        b = e.allocate_batch()
+        e.submit_transfer(b, sp.TransferRequest("s", k * (n // 4), "d", k * (n // 4), n // 4))
+        assert e.await_batch(b).state == sp.BatchState.COMPLETE
+        e.free_batch(b)
+    csv = e.telemetry_csv().strip().splitlines()
+    assert csv[0] == ("window_start_ms,rail_id,bytes_ok,bytes_failed,queue_depth_bytes,p50_us,p99_us,"
+                      "health_state,throughput_gbps")
+    rows = [r.split(",") for r in csv[1:]]
+    assert len(rows) > 0 and len(rows) % 4 == 0  # every window has one row per rail
+    by_rail = {}
+    for r in rows:
+        by_rail[r[1]] = by_rail.get(r[1], 0) + int(r[2])
+        assert int(r[3]) == 0 and r[7] in ("healthy", "excluded", "probing")
+        assert float(r[6]) >= float(r[5]) >= 0.0
+    for i in range(e.rail_count()):
+        assert by_rail.get(e.rail_id(i), 0) == e.rail_stats(i).bytes_ok
+    assert sum(by_rail.values()) == n
+    e.stop()
+
+
 def test_all_rails_down_stall_then_complete_after_probing(co):
     """test_engine.cpp:258-272: every rail down for 100 ms; slices park, the prober
     (1 s cadence, 2 OK probes) reintegrates the rails, the batch completes bit-exact with
