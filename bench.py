@@ -251,15 +251,22 @@ def run_b200(args):
         dist.barrier()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
+    step_t = []
     for _ in range(args.steps):
+        ts = time.perf_counter()
         b = eng.allocate_batch()
         eng.submit_transfers(b, creqs)
         st = eng.await_batch(b)
         if st.state != sp.BatchState.COMPLETE:
             raise RuntimeError(f"e2e batch not complete: {st}")
         eng.free_batch(b)
-    torch.cuda.synchronize()
+        step_t.append((time.perf_counter() - ts) * 1e3)
+    # the step ends when await_batch has read COMPLETE from the mapped counters (published
+    # after the delivered bytes were fenced); a device-wide synchronize here would instead
+    # wait out the persistent kernel's idle-exit timer
     e2e_ms = (time.perf_counter() - t0) * 1e3
+    if os.environ.get("SPRAY_BENCH_DEBUG"):
+        print("e2e step ms:", [round(x, 3) for x in step_t], file=sys.stderr, flush=True)
 
     # ---- state-blind baseline: round-robin cudaMemcpyAsync striping of the same blocks
     # (one call per block from C++, the same interleaved order, 4 streams)

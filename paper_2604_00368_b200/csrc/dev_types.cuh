@@ -171,6 +171,7 @@ struct alignas(64) Control {
   volatile uint64_t idle_exit_ns;
   // device -> host
   volatile uint64_t sub_head;        // intents consumed
+  volatile uint64_t bulk_done;       // bulk intent arrays fully read by the device (in order)
   volatile uint32_t state;           // 0 exited, 1 running, 2 exiting
   volatile uint32_t pad0_;
   volatile uint64_t device_now;      // engine clock (ns since epoch) seen by the scheduler
@@ -212,6 +213,9 @@ struct GateDev {
   uint64_t lo, hi;         // device-usable address range of the segment
   uint32_t* flags;         // per-granule counters (written by the producing engine)
   uint32_t* consumed;      // per-granule consumption counters (CONSUME only, local HBM)
+  uint32_t* produced;      // per-granule production counters (PRODUCE only, local HBM): the
+                           // flag is written as a plain value, so it may live in any memory
+                           // this GPU can store to (peer HBM, mapped pinned host memory)
   uint32_t role;
   uint32_t pad_;
 };

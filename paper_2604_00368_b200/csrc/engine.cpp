@@ -743,13 +743,22 @@ void Engine::gate_segment(const std::string& seg_id, uint32_t role, void* flags)
   g.hi = bf.dev_addr + bf.length;
   g.flags = static_cast<uint32_t*>(flags);
   g.role = role;
-  if (role == kGateConsume) {
+  {  // this engine's own per-granule counters (consumed or produced), zeroed
     CK(cudaSetDevice(device_));
     void* p = nullptr;
     CK(cudaMalloc(&p, granules * sizeof(uint32_t)));
     CK(cudaMemset(p, 0, granules * sizeof(uint32_t)));
     dev_allocs_.push_back(p);
-    g.consumed = static_cast<uint32_t*>(p);
+    if (role == kGateConsume) g.consumed = static_cast<uint32_t*>(p);
+    else g.produced = static_cast<uint32_t*>(p);
+  }
+  // flags may be mapped pinned host memory (a staged route through the host): use the
+  // device alias of such a pointer
+  {
+    cudaPointerAttributes pa{};
+    if (cudaPointerGetAttributes(&pa, flags) == cudaSuccess && pa.type == cudaMemoryTypeHost && pa.devicePointer)
+      g.flags = static_cast<uint32_t*>(pa.devicePointer);
+    cudaGetLastError();
   }
   E_.gates[E_.n_gates++] = g;
   s.gated = true;

@@ -403,6 +403,45 @@ def test_dataflow_gate_forwarding_chain_bit_exact():
     b.stop()
 
 
+def test_staged_route_through_host_memory_bit_exact():
+    """Staged multi-hop route (engine.cpp:465-610 analog): HBM ->
+    pinned host staging -> HBM, pipelined by granule between two engines. The gate
+    counters live in mapped host memory, so the route needs no peer access."""
+    topo = fabrics.kv_offload(DEV)
+    cfg = {"resilience": {"degradation_ratio": 1e9}, "b200": {"chunk_bytes": 65536, "gate_timeout_ms": 20000}}
+    a, b = make_engine(topo, cfg), make_engine(topo, cfg)
+    n = 128 << 20
+    src, dst = dev_buf(n, 57), dev_buf(n)
+    stage = torch.zeros(n, dtype=torch.uint8, pin_memory=True)
+    cb = a.chunk_bytes()
+    flags_p = sp.host_alloc(4 * (n // cb))
+    C.memset(flags_p, 0, 4 * (n // cb))
+    node = f"g{DEV}"
+    for e in (a, b):
+        e.register_segment(sp.SegmentDescriptor("src", sp.Medium.DEVICE, node, [sp.BufferDesc(0, n, src.data_ptr())]))
+        e.register_segment(sp.SegmentDescriptor("stage", sp.Medium.HOST, node, [sp.BufferDesc(0, n, stage.data_ptr())]))
+        e.register_segment(sp.SegmentDescriptor("dst", sp.Medium.DEVICE, node, [sp.BufferDesc(0, n, dst.data_ptr())]))
+    a.gate_segment("stage", sp.Engine.GATE_PRODUCE, flags_p)
+    b.gate_segment("stage", sp.Engine.GATE_CONSUME, flags_p)
+    flags = np.ctypeslib.as_array((C.c_uint32 * (n // cb)).from_address(flags_p))
+    for run in range(2):
+        dst.zero_()
+        torch.cuda.synchronize()
+        bb = b.allocate_batch()
+        b.submit_transfer(bb, sp.TransferRequest("stage", 0, "dst", 0, n))
+        ba = a.allocate_batch()
+        a.submit_transfer(ba, sp.TransferRequest("src", 0, "stage", 0, n))
+        assert a.await_batch(ba, 60_000_000_000).state == sp.BatchState.COMPLETE
+        assert b.await_batch(bb, 60_000_000_000).state == sp.BatchState.COMPLETE
+        a.free_batch(ba)
+        b.free_batch(bb)
+        assert torch.equal(src, dst), run
+        assert int(flags.min()) == run + 1 and int(flags.max()) == run + 1
+    a.stop()
+    b.stop()
+    sp.host_free(flags_p)
+
+
 def test_telemetry_csv_windows_account_every_byte():
     """TelemetrySnapshot::to_csv columns (telemetry.cpp:123-158) from the device window
     cells: per-window bytes sum to the delivered bytes, per rail; percentiles ordered."""
