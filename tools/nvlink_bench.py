@@ -70,6 +70,20 @@ def c2(args):
     best, mean = timed_prepared(e, req, args.reps)
     out["engine_gbs"] = round(n / (best * 1e-3) / 1e9, 2)
     out["engine_gbs_mean"] = round(n / (mean * 1e-3) / 1e9, 2)
+    if args.prof:  # scheduler-warp cycle counters of the last launch (tools/gpu_perf.py names)
+        import ctypes as C
+        from paper_2604_00368_b200 import _lib as L
+        w = (C.c_uint64 * 48)()
+        L.lib.spray_engine_debug(e._h, w, 48)
+        names = ["host_tail", "sub_tail", "sub_head", "state", "now", "disp", "term", "failed", "retried", "trace_n",
+                 "stream", "loops", "serial", "obs", "fb", "n_comp", "n_dec", "apply", "decide", "ctl", "ingress",
+                 "complete", "egress", "egress_blocks", "ingress_blocks", "entries", "pub_busy", "rx_busy",
+                 "n_fences", "p1", "p2", "p3"]
+        d = dict(zip(names, list(w)))
+        out["prof_ms"] = {k: round(d[k] / 1.965e6, 3) for k in ("serial", "obs", "fb", "p1", "p2", "p3", "apply",
+                                                               "decide", "ctl", "ingress", "complete", "egress",
+                                                               "pub_busy")}
+        out["prof_counts"] = {k: d[k] for k in ("loops", "entries", "n_comp", "n_dec", "n_fences")}
     assert sp.checksum(1, dst.data_ptr(), n) == sp.checksum(0, src.data_ptr(), n)
     # e2e through the public API
     t0 = time.perf_counter()
@@ -308,6 +322,7 @@ def main():
     ap.add_argument("--ce-rails", type=int, default=0)
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--fault-after-ms", type=float, default=0.3)
+    ap.add_argument("--prof", action="store_true", help="c2: print scheduler-warp cycle counters")
     args = ap.parse_args()
     out = {"c2": c2, "elephant": elephant, "c4": c4, "c4chain": c4chain, "c5": c5}[args.mode](args)
     print(json.dumps(out), flush=True)
