@@ -211,6 +211,62 @@ def test_large_submit_races_device_completion():
     e.stop()
 
 
+def test_device_decompose_matches_oracle_at_edges(co):
+    """SliceScheduler::decompose (scheduler.cpp:94-106) as the INGRESS warp runs it, at the
+    edges: single bytes, one short of / exactly / one past the minimum slice and its
+    double, the 4096-slice cap (1 GiB -> 256 KiB slices) and a ragged size past the cap.
+    Every DECIDE in the live trace carries the slice's length and absolute source offset."""
+    topo = fabrics.two_node(2, 1e9, backend="cuda")
+    e = make_engine(topo, {"resilience": {"degradation_ratio": 1e9}})
+    e.trace_enable(1 << 16)
+    n = (1 << 30) + (1 << 20)
+    src, dst = dev_buf(n, 19), dev_buf(n)
+    e.register_segment(sp.SegmentDescriptor("s", sp.Medium.DEVICE, "a", [sp.BufferDesc(0, n, src.data_ptr())]))
+    e.register_segment(sp.SegmentDescriptor("d", sp.Medium.DEVICE, "b", [sp.BufferDesc(0, n, dst.data_ptr())]))
+    lens = [1, 4095, 65535, 65536, 65537, 131071, 131072, 131073, (64 << 20) + 3, 1 << 30, (1 << 30) + 12345]
+    offs = [7, 100, 0, 65536, 3, 1 << 20, 0, 11, 5 << 20, 0, 999]
+    b = e.allocate_batch()
+    for ln, off in zip(lens, offs):
+        e.submit_transfer(b, sp.TransferRequest("s", off, "d", off, ln))
+    assert e.await_batch(b, 60_000_000_000).state == sp.BatchState.COMPLETE
+    ev, dec = e.trace_fetch(1 << 16)
+    d = ev[ev["kind"] == 1]
+    k = 0
+    for ln, off in zip(lens, offs):
+        o, l = co.decompose(ln)
+        got = d[k:k + len(o)]
+        assert np.array_equal(got["len"], l), ln
+        assert np.array_equal(got["offset"] - off, o), ln
+        k += len(o)
+    assert k == len(d)
+    for ln, off in zip(lens, offs):
+        assert torch.equal(src[off:off + ln], dst[off:off + ln]), ln
+    e.stop()
+
+
+def test_many_tiny_transfers_in_one_batch_bit_exact():
+    """20000 intents of 1..512 bytes at random (unaligned) offsets in one submit call."""
+    topo = fabrics.two_node(3, [3e9, 2e9, 1e9], backend="cuda")
+    e = make_engine(topo, {"resilience": {"degradation_ratio": 1e9}})
+    n = 32 << 20
+    src, dst = dev_buf(n, 23), dev_buf(n)
+    e.register_segment(sp.SegmentDescriptor("s", sp.Medium.DEVICE, "a", [sp.BufferDesc(0, n, src.data_ptr())]))
+    e.register_segment(sp.SegmentDescriptor("d", sp.Medium.DEVICE, "b", [sp.BufferDesc(0, n, dst.data_ptr())]))
+    rng = np.random.default_rng(99)
+    cells = rng.permutation(n // 1024)[:20000]  # disjoint 1 KiB cells
+    lens = rng.integers(1, 513, size=len(cells))
+    offs = cells * 1024 + rng.integers(0, 512, size=len(cells))
+    b = e.allocate_batch()
+    e.submit_transfers(b, [sp.TransferRequest("s", int(o), "d", int(o), int(l)) for o, l in zip(offs, lens)])
+    assert e.await_batch(b, 60_000_000_000).state == sp.BatchState.COMPLETE
+    mask = torch.zeros(n, dtype=torch.bool)
+    for o, l in zip(offs, lens):
+        mask[int(o):int(o) + int(l)] = True
+    s_, d_ = src.cpu(), dst.cpu()
+    assert torch.equal(s_[mask], d_[mask]) and int((d_[~mask] != 0).sum()) == 0
+    e.stop()
+
+
 # ------------------------------------------------------------------ bytes
 def test_random_transfers_bit_exact():
     """Acceptance criterion 1 analogue: randomized lengths (1 B .. 32 MiB) and offsets,
@@ -304,13 +360,15 @@ def test_batch_api_semantics():
 
 
 # ------------------------------------------------------------------ self-healing
-def test_down_fault_reroutes_with_zero_lost_bytes(co):
+@pytest.mark.parametrize("policy", ["telemetry", "rr", "hash"])
+def test_down_fault_reroutes_with_zero_lost_bytes(co, policy):
     """Disable one of two rails mid-transfer: its in-flight slices fail (partial prefix
     writes), three consecutive failures exclude it (resilience.cpp:71-83), retries land
     on the healthy rail (engine.cpp:405-454); the batch completes bit-exact and the
-    live trace still replays identically."""
+    live trace still replays identically, under every policy."""
     topo = fabrics.two_node(2, 1e9, backend="cuda")
-    e = make_engine(topo, {"resilience": {"degradation_ratio": 1e9}, "b200": {"chunk_bytes": 65536}})
+    e = make_engine(topo, {"resilience": {"degradation_ratio": 1e9}, "b200": {"chunk_bytes": 65536},
+                           "scheduler": {"policy": policy}})
     e.trace_enable(1 << 18)
     n = 256 << 20
     src, dst = dev_buf(n, 11), dev_buf(n)
@@ -334,7 +392,8 @@ def test_down_fault_reroutes_with_zero_lost_bytes(co):
     heal_ms = (h["first_reroute_ok_ns"] - h["fault_start_ns"]) / 1e6
     assert 0 < heal_ms < 50.0
     bw, tier, rank = rails_of(topo)
-    replay_live(co, e, sched_config(), res_config(degradation_ratio=1e9), bw, tier, rank)
+    replay_live(co, e, sched_config(policy={"telemetry": 0, "rr": 1, "hash": 2}[policy]),
+                res_config(degradation_ratio=1e9), bw, tier, rank)
     e.stop()
 
 

@@ -33,10 +33,14 @@ def buf(dev, n, seed=None):
     return t
 
 
+CE_GBS = 770.0  # declared bandwidth of copy-engine rails (--ce-gbs)
+
+
 def engine(dev, gpus, sm_rails, ce_rails, extra_cfg=None):
     cfg = {"resilience": {"degradation_ratio": 1e9}}
     cfg.update(extra_cfg or {})
-    e = sp.Engine(fabrics.peer_fabric(gpus, sm_rails=sm_rails, ce_rails=ce_rails), json.dumps(cfg), dev)
+    e = sp.Engine(fabrics.peer_fabric(gpus, sm_rails=sm_rails, ce_rails=ce_rails, bw_ce=CE_GBS * 1e9),
+                  json.dumps(cfg), dev)
     e.start()
     return e
 
@@ -323,7 +327,10 @@ def main():
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--fault-after-ms", type=float, default=0.3)
     ap.add_argument("--prof", action="store_true", help="c2: print scheduler-warp cycle counters")
+    ap.add_argument("--ce-gbs", type=float, default=770.0, help="declared bandwidth of each copy-engine rail")
     args = ap.parse_args()
+    global CE_GBS
+    CE_GBS = args.ce_gbs
     out = {"c2": c2, "elephant": elephant, "c4": c4, "c4chain": c4chain, "c5": c5}[args.mode](args)
     print(json.dumps(out), flush=True)
     os._exit(0)
