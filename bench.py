@@ -45,6 +45,12 @@ def parse():
     p.add_argument("--ce-rails", type=int, default=0, help="copy-engine rails sprayed beside the SM rail")
     p.add_argument("--ce-gbs", type=float, default=15.0, help="declared bandwidth of each copy-engine rail")
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--lat-batches", type=int, default=200, help="small batches timed for the batch-latency percentiles")
+    p.add_argument("--lat-intents", type=int, default=64, help="intents per latency batch (half offload, half reload)")
+    p.add_argument("--no-congestion", action="store_true")
+    p.add_argument("--no-nvlink", action="store_true", help="N>1: skip the NVLink phase (elephant, broadcast chain, fault)")
+    p.add_argument("--nvl-bytes", type=int, default=1 << 30, help="N>1: bytes per elephant flow (C2 shape)")
+    p.add_argument("--bcast-bytes", type=int, default=16 << 30, help="N>1: broadcast size (C4 shape)")
     return p.parse_args()
 
 
@@ -172,6 +178,294 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(rows)}
 
 
+
+# ------------------------------------------------------------------ batch latency
+def pct(xs, q):
+    """exact_percentile (bench.cpp): the value at rank ceil(q*n) of the sorted sample."""
+    ys = sorted(xs)
+    if not ys:
+        return None
+    k = max(0, min(len(ys) - 1, int(-(-q * len(ys) // 1)) - 1))
+    return ys[k]
+
+
+def batch_latency(sp, eng, reqs, n_batches, per_batch):
+    """P50/P90/P99 batch latency (bench.cpp:156-157, 213-215: submit -> batch terminal) of
+    small KV batches (per_batch intents, offloads and reloads interleaved) through the
+    public API, one batch in flight, as a HiCache prefetch/offload request sees it."""
+    groups = [sp.Requests(reqs[i:i + per_batch]) for i in range(0, len(reqs) - per_batch + 1, per_batch)]
+    lat = []
+    for k in range(n_batches + 10):
+        g = groups[k % len(groups)]
+        t0 = time.perf_counter()
+        b = eng.allocate_batch()
+        eng.submit_transfers(b, g)
+        st = eng.await_batch(b)
+        if st.state != sp.BatchState.COMPLETE:
+            raise RuntimeError(f"latency batch not complete: {st}")
+        eng.free_batch(b)
+        if k >= 10:
+            lat.append((time.perf_counter() - t0) * 1e6)
+    return {"intents_per_batch": per_batch, "bytes_per_batch": sum(r.length for r in reqs[:per_batch]),
+            "batches": len(lat), "p50_us": round(pct(lat, 0.5), 1), "p90_us": round(pct(lat, 0.9), 1),
+            "p99_us": round(pct(lat, 0.99), 1), "mean_us": round(sum(lat) / len(lat), 1)}
+
+
+# ------------------------------------------------------------------ injected congestion
+def congestion(sp, fabrics, dev, hbm, host, nb, blk, perm, reps=4):
+    """Telemetry spraying vs state-blind round robin (Policy::kRoundRobin, a25) on the same
+    two SM rails of this GPU's PCIe root when one rail is congested: a DEGRADE fault
+    (sim_backend.cpp:171-181 semantics on the real fabric: FIFO service at factor x B)
+    throttles g.pcie1 to 10% for the whole run. Workload: the offload half of the KV batch.
+    The cost model only (degradation exclusion off), so the difference is the scheduler's."""
+    out = {"workload": f"{nb} x {blk >> 10} KiB offload HBM->pinned host per batch",
+           "fabric": "2 SM rails on one PCIe root, g.pcie1 DEGRADE factor 0.1",
+           "exclusion": "off (degradation_ratio 1e9): cost-model steering only"}
+    for pol in ("telemetry", "round_robin"):
+        cfg = {"resilience": {"degradation_ratio": 1e9}, "scheduler": {"policy": pol},
+               "b200": {"chunk_bytes": 65536}}
+        e = sp.Engine(fabrics.kv_offload(dev, sm_rails=2), json.dumps(cfg), dev)
+        e.start()
+        node = f"g{dev}"
+        e.register_segment(sp.SegmentDescriptor("c/hbm", sp.Medium.DEVICE, node, [sp.BufferDesc(0, nb * blk, hbm.data_ptr())]))
+        e.register_segment(sp.SegmentDescriptor("c/host", sp.Medium.HOST, node, [sp.BufferDesc(0, nb * blk, host.data_ptr())]))
+        now = e.now_ns()
+        e.inject_fault(f"g{dev}.pcie1", sp.FaultEffect.DEGRADE, now, now + 10 ** 13, 0.1)
+        prep = e.prepare_transfers([sp.TransferRequest("c/hbm", i * blk, "c/host", int(perm[i]) * blk, blk)
+                                    for i in range(nb)])
+        ms = []
+        for k in range(reps + 2):
+            b = e.allocate_batch()
+            t = prep.run(b)
+            if e.batch_status(b).state != sp.BatchState.COMPLETE:
+                raise RuntimeError("congestion batch not complete")
+            e.free_batch(b)
+            if k >= 2:
+                ms.append(t)
+        share = {s.rail_id: s.bytes_ok for s in (e.rail_stats(r) for r in range(e.rail_count())) if s.bytes_ok}
+        tot = sum(share.values()) or 1
+        out[pol] = {"gbs": round(nb * blk / (statistics.mean(ms) * 1e-3) / 1e9, 3),
+                    "ms_per_batch": round(statistics.mean(ms), 3),
+                    "bytes_share": {k: round(v / tot, 4) for k, v in share.items()}}
+        prep.free()
+        e.stop()
+    out["telemetry_over_rr"] = round(out["telemetry"]["gbs"] / out["round_robin"]["gbs"], 3)
+    return out
+
+
+# ------------------------------------------------------------------ NVLink phase (N > 1)
+def nvlink_phase(sp, fabrics, args, rank, world, dev):
+    """The NVLink configurations at N GPUs, one process per GPU, peer HBM shared through CUDA
+    IPC handles (exchanged over torch.distributed: handles, barriers and max-over-ranks
+    timing only; no data-path collective). Every time is the engine kernel's CUDA-event
+    time on its own stream, max over ranks.
+      elephant  C2 x N: N disjoint flows rank r -> r+1 (mod N), nvl_bytes each, 4096 slices
+      bcast     C4: bcast_bytes from rank 0 to every other rank as a pipelined chain
+                0 -> 1 -> ... -> N-1 (dataflow gates), vs rank 0 fanning out alone
+      fault     C5: rank 0's flow loses its direct SM rail mid-transfer (DOWN) while every
+                other flow keeps running (background load); alternate = copy-engine rail
+    Delivered bytes are checked by device checksums against the senders'."""
+    import torch
+    import torch.distributed as dist
+    GBs = lambda b, ms: round(b / (ms * 1e-3) / 1e9, 2)  # noqa: E731
+    out = {"ranks": world}
+    nxt, prv = (rank + 1) % world, (rank - 1) % world
+    opened = {}
+
+    def gather(obj):
+        objs = [None] * world
+        dist.all_gather_object(objs, obj)
+        return objs
+
+    def maxr(x):
+        t = torch.tensor([float(x)], dtype=torch.float64, device=f"cuda:{dev}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def allok(x):
+        t = torch.tensor([0.0 if x else 1.0], dtype=torch.float64, device=f"cuda:{dev}")
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        return float(t.item()) == 0.0
+
+    def open_peer(h):  # one mapping per exported allocation
+        if h not in opened:
+            opened[h] = sp.ipc_open(dev, h)
+        return opened[h]
+
+    def seg(e, sid, g, n, ptr):
+        e.register_segment(sp.SegmentDescriptor(sid, sp.Medium.DEVICE, f"g{g}", [sp.BufferDesc(0, n, ptr)]))
+
+    # ---- elephant flows
+    n = args.nvl_bytes
+    src = torch.empty(n, dtype=torch.uint8, device=f"cuda:{dev}")
+    sp.fill_splitmix(dev, src.data_ptr(), n, 500 + rank)
+    dst = torch.zeros(n, dtype=torch.uint8, device=f"cuda:{dev}")
+    hs = gather(sp.ipc_export(dev, dst.data_ptr()))
+    pdst = open_peer(hs[nxt])
+    cfg = json.dumps({"resilience": {"degradation_ratio": 1e9}})
+    e = sp.Engine(fabrics.peer_fabric(sorted({rank, nxt})), cfg, dev)
+    e.start()
+    seg(e, f"src{rank}", rank, n, src.data_ptr())
+    seg(e, f"dst{nxt}", nxt, n, pdst)
+    prep = e.prepare_transfers([sp.TransferRequest(f"src{rank}", 0, f"dst{nxt}", 0, n)])
+    times = []
+    for k in range(args.warmup + max(3, args.steps)):
+        torch.cuda.synchronize(dev)
+        dist.barrier()
+        b = e.allocate_batch()
+        ms = prep.run(b)
+        ok = e.batch_status(b).state == sp.BatchState.COMPLETE
+        e.free_batch(b)
+        ms = maxr(ms if ok else 1e9)
+        if k >= args.warmup:
+            times.append(ms)
+    torch.cuda.synchronize(dev)
+    dist.barrier()
+    sums = gather(sp.checksum(dev, src.data_ptr(), n))
+    exact = allok(sp.checksum(dev, dst.data_ptr(), n) == sums[prv])
+    mean = statistics.mean(times)
+    out["elephant"] = {"flows": f"{world} x (r -> r+1 mod {world})", "bytes_per_flow": n, "slices_per_flow": 4096,
+                       "rails": "1 SM peer-store rail per GPU", "ms_max_over_ranks": round(mean, 4),
+                       "aggregate_gbs": GBs(world * n, mean), "per_flow_gbs": GBs(n, mean),
+                       "best_aggregate_gbs": GBs(world * n, min(times)),
+                       "roofline": {"peak_gbs": 900.0 * world, "unit": "GB/s",
+                                    "frac": round(world * n / (mean * 1e-3) / 1e9 / (900.0 * world), 4),
+                                    "peak_source": "nominal NVLink 5, 900 GB/s per direction per GPU"},
+                       "bit_exact": exact}
+    prep.free()
+    e.stop()
+
+    # ---- broadcast: pipelined chain vs fan-out from rank 0
+    nb_ = args.bcast_bytes
+    w = torch.empty(nb_, dtype=torch.uint8, device=f"cuda:{dev}")
+    if rank == 0:
+        sp.fill_splitmix(dev, w.data_ptr(), nb_, 4242)
+    else:
+        w.zero_()
+    chain_cfg = json.dumps({"resilience": {"degradation_ratio": 1e9}})
+    cb = 65536
+    flags = torch.zeros(nb_ // cb, dtype=torch.int32, device=f"cuda:{dev}")
+    hs = gather((sp.ipc_export(dev, w.data_ptr()), sp.ipc_export(dev, flags.data_ptr())))
+    ec, pc = None, None
+    if rank + 1 < world:
+        pw, pf = open_peer(hs[rank + 1][0]), open_peer(hs[rank + 1][1])
+        ec = sp.Engine(fabrics.peer_fabric(sorted({rank, rank + 1})), chain_cfg, dev)
+        ec.start()
+        seg(ec, f"w{rank}", rank, nb_, w.data_ptr())
+        seg(ec, f"w{rank + 1}", rank + 1, nb_, pw)
+        ec.gate_segment(f"w{rank + 1}", sp.Engine.GATE_PRODUCE, pf)
+        if rank > 0:
+            ec.gate_segment(f"w{rank}", sp.Engine.GATE_CONSUME, flags.data_ptr())
+        pc = ec.prepare_transfers([sp.TransferRequest(f"w{rank}", 0, f"w{rank + 1}", 0, nb_)])
+    ctimes = []
+    for k in range(3):
+        if rank > 0:
+            w.zero_()
+        torch.cuda.synchronize(dev)
+        dist.barrier()
+        ms = 0.0
+        if pc:
+            b = ec.allocate_batch()
+            ms = pc.run(b)
+            if ec.batch_status(b).state != sp.BatchState.COMPLETE:
+                ms = 1e9
+            ec.free_batch(b)
+        ms = maxr(ms)
+        if k:
+            ctimes.append(ms)
+    torch.cuda.synchronize(dev)
+    dist.barrier()
+    ref = gather(sp.checksum(dev, w.data_ptr(), nb_) if rank == 0 else None)[0]
+    exact = allok(sp.checksum(dev, w.data_ptr(), nb_) == ref)
+    if ec:
+        pc.free()
+        ec.stop()
+    # fan-out: rank 0 alone writes into every peer
+    ftime = None
+    w.zero_() if rank > 0 else None
+    torch.cuda.synchronize(dev)
+    dist.barrier()
+    if rank == 0:
+        peers = [open_peer(hs[j][0]) for j in range(1, world)]
+        ef = sp.Engine(fabrics.peer_fabric(list(range(world))), chain_cfg, dev)
+        ef.start()
+        seg(ef, "w0", 0, nb_, w.data_ptr())
+        for j, p in enumerate(peers, start=1):
+            seg(ef, f"w{j}", j, nb_, p)
+        pf_ = ef.prepare_transfers([sp.TransferRequest("w0", 0, f"w{j}", 0, nb_) for j in range(1, world)])
+        b = ef.allocate_batch()
+        ftime = pf_.run(b)
+        if ef.batch_status(b).state != sp.BatchState.COMPLETE:
+            ftime = None
+        ef.free_batch(b)
+        pf_.free()
+        ef.stop()
+    torch.cuda.synchronize(dev)
+    dist.barrier()
+    fexact = allok(sp.checksum(dev, w.data_ptr(), nb_) == ref)
+    cm = statistics.mean(ctimes)
+    out["bcast"] = {"bytes": nb_, "receivers": world - 1, "dtype": "bf16 bit patterns moved as bytes",
+                    "chain_ms": round(cm, 3), "chain_delivered_gbs": GBs((world - 1) * nb_, cm),
+                    "chain_per_receiver_gbs": GBs(nb_, cm), "chain_bit_exact": exact,
+                    "fanout_ms": round(ftime, 3) if ftime else None,
+                    "fanout_delivered_gbs": GBs((world - 1) * nb_, ftime) if ftime else None,
+                    "fanout_bit_exact": fexact,
+                    "ideal_pipelined_ms": round(nb_ / 900e9 * 1e3, 3),
+                    "ideal_fanout_ms": round((world - 1) * nb_ / 900e9 * 1e3, 3)}
+    del w, flags
+    torch.cuda.empty_cache()
+
+    # ---- fault under load: rank 0's direct rail DOWN mid-transfer; others keep flowing
+    dst.zero_()
+    torch.cuda.synchronize(dev)
+    dist.barrier()
+    ce_gbs = 60e9  # the copy-engine rail's declared bandwidth (per-slice host issue bound)
+    # link-down handling only (failure_threshold exclusion + re-spray); the cost model's
+    # degradation exclusion stays off as in the other phases
+    ef = sp.Engine(fabrics.peer_fabric(sorted({rank, nxt}), sm_rails=1, ce_rails=1 if rank == 0 else 0, bw_ce=ce_gbs),
+                   cfg, dev)
+    ef.start()
+    seg(ef, f"src{rank}", rank, n, src.data_ptr())
+    seg(ef, f"dst{nxt}", nxt, n, pdst)
+    req = sp.TransferRequest(f"src{rank}", 0, f"dst{nxt}", 0, n)
+    heal, state = None, None
+    dist.barrier()
+    if rank == 0:
+        b = ef.allocate_batch()
+        ef.submit_transfer(b, req)
+        time.sleep(0.3e-3)
+        now = ef.now_ns()
+        ef.inject_fault(f"g{rank}.nvl0", sp.FaultEffect.DOWN, now, now + 10 ** 13, 0.0)
+        st = ef.await_batch(b, 60_000_000_000)
+        state = st.state.name
+        ef.free_batch(b)
+        heal = ef.heal_stats()
+        rails = {s.rail_id: {"bytes_ok": s.bytes_ok, "bytes_failed": s.bytes_failed, "health": s.health.name}
+                 for s in (ef.rail_stats(r) for r in range(ef.rail_count()))}
+    else:
+        for _ in range(4):  # background flows
+            b = ef.allocate_batch()
+            ef.submit_transfer(b, req)
+            ef.await_batch(b, 60_000_000_000)
+            ef.free_batch(b)
+    torch.cuda.synchronize(dev)
+    dist.barrier()
+    exact = allok(sp.checksum(dev, dst.data_ptr(), n) == sums[prv])
+    ef.stop()
+    if rank == 0:
+        hm = None
+        if heal and heal["first_reroute_ok_ns"] and heal["fault_start_ns"]:
+            hm = round((heal["first_reroute_ok_ns"] - heal["fault_start_ns"]) / 1e6, 3)
+        out["fault"] = {"what": f"g0.nvl0 DOWN 0.3 ms into a {n >> 20} MiB flow 0 -> 1 while the other "
+                                f"{world - 1} flow(s) run; alternate = copy-engine rail g0.ce0",
+                        "state": state, "heal_ms": hm, "failed_attempts": heal["failed_attempts"],
+                        "retried_ok": heal["retried_ok"], "rails": rails, "all_flows_bit_exact": exact,
+                        "target_ms": 50}
+    for p in opened.values():
+        sp.ipc_close(p)
+    return out
+
+
 # ------------------------------------------------------------------ B200 arm
 def run_b200(args):
     import numpy as np
@@ -268,6 +562,9 @@ def run_b200(args):
     if os.environ.get("SPRAY_BENCH_DEBUG"):
         print("e2e step ms:", [round(x, 3) for x in step_t], file=sys.stderr, flush=True)
 
+    e2e_step_ms = step_t
+    lat = batch_latency(sp, eng, reqs, args.lat_batches, args.lat_intents) if args.lat_batches else None
+
     # ---- state-blind baseline: round-robin cudaMemcpyAsync striping of the same blocks
     # (one call per block from C++, the same interleaved order, 4 streams)
     hb0, hs0, h20, hb20 = hbm.data_ptr(), host.data_ptr(), host2.data_ptr(), hbm2.data_ptr()
@@ -289,6 +586,21 @@ def run_b200(args):
     if world > 1:
         dist.all_reduce(vals, op=dist.ReduceOp.MAX)
     total_ms, e2e_ms, rr_ms = vals.tolist()
+    eng.stop()
+
+    cong = None
+    if rank == 0 and not args.no_congestion:
+        try:
+            cong = congestion(sp, fabrics, dev, hbm, host, nb, blk, p_off)
+        except Exception as ex:  # reported, never fatal
+            cong = {"error": str(ex)[:300]}
+    nvl = None
+    if world > 1 and not args.no_nvlink:
+        try:
+            del hbm2, host2
+            nvl = nvlink_phase(sp, fabrics, args, rank, world, dev)
+        except Exception as ex:  # reported, never fatal
+            nvl = {"error": f"{type(ex).__name__}: {str(ex)[:300]}"}
 
     if rank == 0:
         value = world * args.steps * step_bytes / (total_ms * 1e-3) / 1e9
@@ -336,9 +648,19 @@ def run_b200(args):
             "rr_baseline": {"value": round(world * step_bytes / (rr_ms * 1e-3) / 1e9, 3), "unit": "GB/s",
                             "what": "state-blind round-robin striping: one cudaMemcpyAsync per block from C++ "
                                     "(spray_rr_copy), 4 streams, same blocks and order"},
+            "batch_latency": {"kv_batch_8192_intents": {"p50_ms": round(pct(e2e_step_ms, 0.5), 3),
+                                                        "p90_ms": round(pct(e2e_step_ms, 0.9), 3),
+                                                        "steps": len(e2e_step_ms)},
+                              "small_batches": lat,
+                              "how": "submit -> batch terminal through the public C-ABI, one batch in flight; "
+                                     "exact_percentile as bench.cpp:213-215"},
             "gpu_launches": 2 * args.steps,
             "clocks": clk.summary(),
         }
+        if cong is not None:
+            line["congestion"] = cong
+        if nvl is not None:
+            line["nvlink"] = nvl
         if world == 1 and not args.no_cpu_baseline:
             try:
                 r = reference_kv(nb, blk, 10.0, 2)
@@ -352,7 +674,6 @@ def run_b200(args):
             except Exception as ex:  # reported, never fatal
                 line["cpu_baseline"] = {"value": None, "error": str(ex)}
         print(json.dumps(line), flush=True)
-    eng.stop()
     if world > 1:
         dist.destroy_process_group()
 
