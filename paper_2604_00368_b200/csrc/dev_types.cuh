@@ -29,7 +29,7 @@ struct RailDesc {
   uint32_t executor;      // kExec*
   int32_t gpu;            // owning GPU ordinal (-1 for host-side rails)
   int32_t via;            // relay GPU (relay rails)
-  uint32_t ce_index;      // CE proxy stream index (CE rails)
+  uint32_t ce_index;      // CE proxy stream index (CE rails); relay index (relay rails)
   uint8_t n_partners;     // probe counterparts, affinity partner first (resilience.cpp:17-44)
   uint8_t partners[15];
 };
@@ -220,6 +220,27 @@ struct GateDev {
   uint32_t pad_;
 };
 
+// 2-hop relay rail (executor "relay", via GPU K). Hop 1: this engine's copy workers move a
+// chunk into a staging slot in K's HBM and publish a descriptor there; hop 2: a forwarder
+// kernel running on K's SMs moves it to the destination and does the chunk's completion
+// accounting in this engine's counters (peer atomics), so to the scheduler a relay chunk
+// completes like any other chunk. Tickets restart at 0 every launch (the prologue clears
+// `tail` and `seq`); descriptor stamps carry the launch generation.
+constexpr int kMaxRelays = 8;
+struct RelayDesc {  // 32 B, in K's HBM: written by the hop-1 worker, read by the forwarder
+  uint64_t dst;
+  uint32_t len, slice, target, pad_;
+  uint64_t stamp;   // (launch_gen << 32) | (ticket + 1), release-stored last
+};
+struct RelayDev {
+  uint8_t* staging;             // K's HBM: n_slots x chunk_bytes
+  RelayDesc* desc;              // K's HBM: n_slots descriptors
+  uint32_t* exit_gen;           // K's HBM: the engine writes its launch generation on exit
+  uint32_t* seq;                // this GPU's HBM: per-slot free round (forwarder -> workers)
+  unsigned long long* tail;     // this GPU's HBM: hop-1 ticket counter (workers)
+  uint32_t n_slots, via;        // power of two; relay GPU ordinal
+};
+
 // Everything the kernel needs, passed by value.
 struct EngineDev {
   Control* ctl;                      // mapped host
@@ -269,6 +290,9 @@ struct EngineDev {
   GateDev gates[kMaxGates];
   TeleCell* tele;                              // HBM [n_rails][kTeleWindows] telemetry windows
   uint64_t window_ns;                          // telemetry window (stats_window_ms, default 10 ms)
+  RelayDev relays[kMaxRelays];                 // relay rails (RailDesc::ce_index = relay index)
+  uint32_t n_relays;
+  uint32_t launch_gen;                         // bumped by the host on every launch
 };
 
 // scalars persisted in EngineDev::persist between launches

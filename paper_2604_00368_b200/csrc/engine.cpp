@@ -13,6 +13,7 @@ namespace spray_launch {
 size_t engine_smem_bytes();
 cudaError_t launch_engine(const spray_dev::EngineDev& E, int grid, int block, cudaStream_t st);
 cudaError_t launch_epoch(uint64_t* out, cudaStream_t st);
+cudaError_t launch_relay_forward(const spray_dev::EngineDev& E, uint32_t r, cudaStream_t st);
 }  // namespace spray_launch
 
 namespace spray {
@@ -205,7 +206,8 @@ Engine::Engine(EngineOptions opts, const std::string& topology_json, int device)
   if (topo_.rail_count() > size_t(kMaxRails)) throw ConfigError("topology: more than 64 rails per engine");
   for (RailIndex i = 0; i < topo_.rail_count(); ++i) {
     const RailDecl& r = topo_.rail(i);
-    if (r.executor == 2) throw ConfigError("rail '" + r.id + "': relay executor requires the multi-GPU runtime");
+    if (r.executor == 2 && r.via < 0)
+      throw ConfigError("rail '" + r.id + "': relay executor needs \"via\" (the relay GPU ordinal)");
     if (r.executor == 1) {
       has_ce_ = true;
       if (r.ce_index >= 8) throw ConfigError("rail '" + r.id + "': ce_index must be < 8");
@@ -290,6 +292,7 @@ void Engine::alloc_device() {
   std::vector<RailDesc> rd(nr);
   std::vector<RailState> rs(nr);
   const auto ranks = topo_.id_ranks();
+  std::vector<std::pair<uint32_t, int>> relay_rails;  // (relay index, via GPU)
   for (uint32_t i = 0; i < nr; ++i) {
     const RailDecl& r = topo_.rail(i);
     rd[i] = RailDesc{};
@@ -300,6 +303,11 @@ void Engine::alloc_device() {
     rd[i].gpu = r.gpu;
     rd[i].via = r.via;
     rd[i].ce_index = r.ce_index;
+    if (r.executor == 2) {
+      if (relay_rails.size() >= size_t(kMaxRelays)) throw ConfigError("more than 8 relay rails");
+      rd[i].ce_index = static_cast<uint32_t>(relay_rails.size());
+      relay_rails.emplace_back(rd[i].ce_index, r.via);
+    }
     // probe counterparts (resilience.cpp:17-44): same-backend rails on other nodes, the
     // 1:1 affinity partner first, nodes in id order; node-local backends probe themselves
     {
@@ -411,13 +419,89 @@ void Engine::alloc_device() {
   CK(cudaStreamSynchronize(copy_stream_));
   ctl_->epoch = E_.epoch;
   ctl_->idle_exit_ns = opts_.idle_exit_ns;
+  for (const auto& rr : relay_rails) setup_relay(rr.first, rr.second);
+  E_.n_relays = static_cast<uint32_t>(relay_rails.size());
   if (has_ce_) {
     ce_streams_.resize(8);
     for (auto& s : ce_streams_) CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
   }
 }
 
+// A relay rail's state: staging slots, descriptors and the exit generation in the relay
+// GPU's HBM (hop 2 reads them locally), the slot-free rounds and the ticket counter here
+// (hop 1 polls them locally). Peer access: this GPU <-> via both ways (staging stores,
+// completion atomics), via -> every other GPU it can reach (hop-2 destinations).
+void Engine::setup_relay(uint32_t idx, int via) {
+  int n = 0;
+  CK(cudaGetDeviceCount(&n));
+  if (via >= n) throw ConfigError("relay rail: via GPU " + std::to_string(via) + " does not exist");
+  int a = 1, b = 1;
+  if (via != device_) {
+    CK(cudaDeviceCanAccessPeer(&a, device_, via));
+    CK(cudaDeviceCanAccessPeer(&b, via, device_));
+  }
+  if (!a || !b) throw ConfigError("relay rail: no peer access between GPU " + std::to_string(device_) + " and " +
+                                  std::to_string(via));
+  auto enable = [](int peer) {
+    const cudaError_t e = cudaDeviceEnablePeerAccess(peer, 0);
+    if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) CK(e);
+    cudaGetLastError();
+  };
+  CK(cudaSetDevice(device_));
+  if (via != device_) enable(via);
+  CK(cudaSetDevice(via));
+  for (int j = 0; j < n; ++j) {
+    int ok = 0;
+    if (j != via && cudaDeviceCanAccessPeer(&ok, via, j) == cudaSuccess && ok) enable(j);
+  }
+  RelayHost h;
+  h.via = via;
+  CK(cudaStreamCreateWithFlags(&h.stream, cudaStreamNonBlocking));
+  constexpr uint32_t kSlots = 1024;  // a multiple of the forwarder's 512 warps
+  RelayDev R{};
+  R.n_slots = kSlots;
+  R.via = static_cast<uint32_t>(via);
+  auto on_via = [&](size_t bytes) -> void* {
+    void* p = nullptr;
+    CK(cudaMalloc(&p, bytes));
+    CK(cudaMemset(p, 0, bytes));
+    h.via_allocs.push_back(p);
+    return p;
+  };
+  R.staging = static_cast<uint8_t*>(on_via(size_t(kSlots) << E_.chunk_shift));
+  R.desc = static_cast<RelayDesc*>(on_via(sizeof(RelayDesc) * kSlots));
+  R.exit_gen = static_cast<uint32_t*>(on_via(sizeof(uint32_t)));
+  CK(cudaSetDevice(device_));
+  R.seq = static_cast<uint32_t*>(nullptr);
+  void* p = nullptr;
+  CK(cudaMalloc(&p, sizeof(uint32_t) * kSlots));
+  CK(cudaMemset(p, 0, sizeof(uint32_t) * kSlots));
+  dev_allocs_.push_back(p);
+  R.seq = static_cast<uint32_t*>(p);
+  CK(cudaMalloc(&p, sizeof(unsigned long long)));
+  CK(cudaMemset(p, 0, sizeof(unsigned long long)));
+  dev_allocs_.push_back(p);
+  R.tail = static_cast<unsigned long long*>(p);
+  E_.relays[idx] = R;
+  if (relays_.size() <= idx) relays_.resize(idx + 1);
+  relays_[idx] = std::move(h);
+}
+
+// Every forwarder of the previous launch has returned (each exits once the engine kernel
+// has published its exit generation).
+void Engine::sync_relays() {
+  for (RelayHost& h : relays_)
+    if (h.stream) CK(cudaStreamSynchronize(h.stream));
+}
+
 void Engine::free_device() {
+  for (RelayHost& h : relays_) {
+    cudaSetDevice(h.via);
+    if (h.stream) cudaStreamSynchronize(h.stream), cudaStreamDestroy(h.stream);
+    for (void* p : h.via_allocs) cudaFree(p);
+  }
+  relays_.clear();
+  cudaSetDevice(device_);
   for (void* p : dev_allocs_) cudaFree(p);
   dev_allocs_.clear();
   for (void* p : {static_cast<void*>(ctl_), static_cast<void*>(ring_), static_cast<void*>(bmirror_),
@@ -463,6 +547,8 @@ void Engine::stop() {
   ctl_->stop = 1;
   std::atomic_thread_fence(std::memory_order_seq_cst);
   cudaStreamSynchronize(stream_);
+  for (RelayHost& h : relays_)
+    if (h.stream) cudaStreamSynchronize(h.stream);
   ctl_->stop = 0;
   ctl_->state = 0;
   if (has_ce_) {
@@ -488,12 +574,22 @@ void Engine::launch() {
     // posted-write backlog that every fence and L2 access then waits behind
     // (profiles/pcie_peak.json: 1184 writers -> 72 us fences, 21 us L2 reads).
     if (host_only_sm_) grid = std::min(grid, 1 + kHostLinkCtas);
+    // this GPU relays for others: leave 16 SMs to the forwarders (64 CTAs, 4 per SM)
+    for (RailIndex i = 0; i < topo_.rail_count(); ++i)
+      if (topo_.rail(i).executor == 2 && topo_.rail(i).via == device_) grid = std::min(grid, sms - 16);
   }
   ctl_->stop = 0;
   ctl_->drain = drain_ ? 1u : 0u;
   ctl_->state = 1;
   std::atomic_thread_fence(std::memory_order_seq_cst);
+  sync_relays();
+  E_.launch_gen = ++launch_gen_;
   CK(spray_launch::launch_engine(E_, grid, opts_.block, stream_));
+  for (uint32_t r = 0; r < relays_.size(); ++r) {  // hop 2 on each relay GPU
+    CK(cudaSetDevice(relays_[r].via));
+    CK(spray_launch::launch_relay_forward(E_, r, relays_[r].stream));
+  }
+  if (!relays_.empty()) CK(cudaSetDevice(device_));
 }
 
 bool Engine::running_kernel() { return ctl_ && ctl_->state != 0; }

@@ -175,6 +175,17 @@ class Engine {
   std::atomic<uint64_t> xc_reserve_{0};  // next CE completion ring position (proxy threads)
   std::vector<cudaStream_t> ce_streams_;
   bool has_ce_ = false;
+
+  // 2-hop relay rails: state on the relay GPU, one forwarder kernel per relay and launch
+  struct RelayHost {
+    int via = -1;
+    cudaStream_t stream = nullptr;    // on the relay GPU
+    std::vector<void*> via_allocs;    // staging, descriptors, exit generation
+  };
+  std::vector<RelayHost> relays_;
+  uint32_t launch_gen_ = 0;
+  void setup_relay(uint32_t idx, int via);
+  void sync_relays();
   bool host_only_sm_ = false;  // every SM rail stages through pinned host memory
   static constexpr int kHostLinkCtas = 48;
 };

@@ -40,11 +40,17 @@ def kv_offload(gpu: int = 0, sm_rails: int = 1, ce_rails: int = 0, bw_sm: float 
 
 
 def peer_fabric(gpus: List[int], sm_rails: int = 1, ce_rails: int = 0, bw_sm: float = NVLINK5,
-                bw_ce: float = NVLINK5, extra: Optional[List[Dict]] = None) -> str:
-    """NVLink fabric: one node per GPU, each with `sm_rails` SM peer-store rails (tier 1)
-    and `ce_rails` copy-engine rails, identical ids on every GPU (gK.nvlI / gK.ceI)."""
+                bw_ce: float = NVLINK5, extra: Optional[List[Dict]] = None, relay_via: Optional[List[int]] = None,
+                relay_affinity: str = "same_socket", bw_relay: float = NVLINK5) -> str:
+    """NVLink fabric: one node per GPU, each with `sm_rails` SM peer-store rails (tier 1),
+    `ce_rails` copy-engine rails and one 2-hop relay rail per GPU in `relay_via` (tier 2 by
+    default: the reference's spillover tier), identical ids on every GPU (gK.nvlI / gK.ceI /
+    gK.rlV) so the affinity pairing pairs like with like."""
     rails = []
     for g in gpus:
+        for v in relay_via or []:
+            rails.append({"id": f"g{g}.rl{v}", "node": f"g{g}", "bandwidth_bytes_per_sec": bw_relay,
+                          "affinity": relay_affinity, "backend": "cuda", "executor": "relay", "via": v, "gpu": g})
         for i in range(sm_rails):
             rails.append({"id": f"g{g}.nvl{i}", "node": f"g{g}", "bandwidth_bytes_per_sec": bw_sm,
                           "affinity": "direct", "backend": "cuda", "executor": "sm", "gpu": g})

@@ -1,0 +1,153 @@
+"""2-hop relay rails (executor "relay"): hop 1 by this engine's copy workers into a staging
+slot in the relay GPU's HBM, hop 2 by a forwarder kernel on the relay GPU, which does the
+chunk's completion accounting in the engine's counters. Bytes must be bit-exact whatever
+the mix of rails, across kernel relaunches, and when the direct rail fails mid-transfer
+(the relay is then the alternate path).
+
+Needs >= 2 GPUs (with 2 the relay GPU is the destination GPU itself: hop 2 is a local
+HBM copy there; with >= 3 it is a third GPU)."""
+import json
+
+import pytest
+
+torch = pytest.importorskip("torch")
+
+import paper_2604_00368_b200 as sp  # noqa: E402
+from paper_2604_00368_b200 import fabrics  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+
+def ngpu():
+    return torch.cuda.device_count() if torch.cuda.is_available() else 0
+
+
+needs2 = pytest.mark.skipif(ngpu() < 2, reason="needs 2 GPUs")
+
+
+def via_gpu():
+    return 2 if ngpu() >= 3 else 1
+
+
+def buf(dev, n, seed=None):
+    t = torch.zeros(n, dtype=torch.uint8, device=f"cuda:{dev}")
+    if seed is not None:
+        sp.fill_splitmix(dev, t.data_ptr(), n, seed)
+    return t
+
+
+def engine(topo, cfg=None, dev=0):
+    base = {"resilience": {"degradation_ratio": 1e9}}
+    base.update(cfg or {})
+    e = sp.Engine(topo, json.dumps(base), dev)
+    e.start()
+    return e
+
+
+def seg(e, sid, g, t):
+    e.register_segment(sp.SegmentDescriptor(sid, sp.Medium.DEVICE, f"g{g}", [sp.BufferDesc(0, t.numel(), t.data_ptr())]))
+
+
+def bytes_by_rail(e):
+    return {e.rail_id(r): e.rail_stats(r).bytes_ok for r in range(e.rail_count())}
+
+
+@needs2
+def test_relay_only_random_transfers_bit_exact():
+    """Every slice crosses the relay GPU: random offsets and lengths (unaligned heads and
+    tails, sub-chunk and multi-chunk slices), one batch."""
+    v = via_gpu()
+    e = engine(fabrics.peer_fabric([0, 1], sm_rails=0, relay_via=[v], relay_affinity="direct"))
+    n = 64 << 20
+    src, dst = buf(0, n, 31), buf(1, n)
+    seg(e, "s", 0, src)
+    seg(e, "d", 1, dst)
+    g = torch.Generator().manual_seed(5)
+    reqs, cover = [], torch.zeros(n, dtype=torch.bool)
+    for _ in range(48):
+        off = int(torch.randint(0, n - 1, (1,), generator=g))
+        ln = int(torch.randint(1, min(3 << 20, n - off) + 1, (1,), generator=g))
+        reqs.append(sp.TransferRequest("s", off, "d", off, ln))
+        cover[off:off + ln] = True
+    b = e.allocate_batch()
+    e.submit_transfers(b, reqs)
+    assert e.await_batch(b, 60_000_000_000).state == sp.BatchState.COMPLETE
+    s_, d_ = src.cpu(), dst.cpu()
+    assert torch.equal(d_[cover], s_[cover])
+    assert not d_[~cover].any()
+    assert bytes_by_rail(e)[f"g0.rl{v}"] > 0
+    e.stop()
+
+
+@needs2
+def test_direct_and_relay_sprayed_together_bit_exact():
+    """A tier-1 SM rail and a tier-1 relay rail share one elephant flow: the scheduler
+    sprays slices over both and the delivered bytes are exact."""
+    v = via_gpu()
+    e = engine(fabrics.peer_fabric([0, 1], sm_rails=1, relay_via=[v], relay_affinity="direct"))
+    n = 256 << 20
+    src, dst = buf(0, n, 32), buf(1, n)
+    seg(e, "s", 0, src)
+    seg(e, "d", 1, dst)
+    for _ in range(3):
+        b = e.allocate_batch()
+        e.submit_transfer(b, sp.TransferRequest("s", 0, "d", 0, n))
+        assert e.await_batch(b, 60_000_000_000).state == sp.BatchState.COMPLETE
+        e.free_batch(b)
+    assert sp.checksum(1, dst.data_ptr(), n) == sp.checksum(0, src.data_ptr(), n)
+    by = bytes_by_rail(e)
+    assert by["g0.nvl0"] > 0 and by[f"g0.rl{v}"] > 0
+    e.stop()
+
+
+@needs2
+def test_relay_across_kernel_relaunches():
+    """The persistent kernel exits when idle and relaunches on the next submit; relay
+    tickets restart and the forwarder follows each launch generation."""
+    v = via_gpu()
+    e = engine(fabrics.peer_fabric([0, 1], sm_rails=0, relay_via=[v], relay_affinity="direct"),
+               {"b200": {"idle_exit_ms": 1}})
+    n = 16 << 20
+    src = buf(0, n, 33)
+    import time
+    for k in range(6):
+        dst = buf(1, n)
+        seg(e, f"d{k}", 1, dst)
+        if k == 0:
+            seg(e, "s", 0, src)
+        b = e.allocate_batch()
+        e.submit_transfer(b, sp.TransferRequest("s", 0, f"d{k}", 0, n))
+        assert e.await_batch(b, 30_000_000_000).state == sp.BatchState.COMPLETE
+        e.free_batch(b)
+        assert sp.checksum(1, dst.data_ptr(), n) == sp.checksum(0, src.data_ptr(), n)
+        time.sleep(0.01)  # past the idle exit: the next submit relaunches
+    e.stop()
+
+
+@needs2
+def test_direct_rail_down_reroutes_over_relay():
+    """C5 with a relay alternate: the direct SM rail goes DOWN mid-transfer; its slices
+    fail, the rail is excluded and the retries cross the relay GPU. Zero lost bytes, heal
+    well under 50 ms."""
+    v = via_gpu()
+    e = engine(fabrics.peer_fabric([0, 1], sm_rails=1, relay_via=[v]))
+    n = 1 << 30
+    src, dst = buf(0, n, 34), buf(1, n)
+    seg(e, "s", 0, src)
+    seg(e, "d", 1, dst)
+    b0 = e.allocate_batch()
+    e.submit_transfer(b0, sp.TransferRequest("s", 0, "d", 0, 1 << 20))
+    e.await_batch(b0)
+    b = e.allocate_batch()
+    e.submit_transfer(b, sp.TransferRequest("s", 0, "d", 0, n))
+    now = e.now_ns()
+    e.inject_fault("g0.nvl0", sp.FaultEffect.DOWN, now + 300_000, now + 60_000_000_000)
+    st = e.await_batch(b, 60_000_000_000)
+    assert st.state == sp.BatchState.COMPLETE
+    assert sp.checksum(1, dst.data_ptr(), n) == sp.checksum(0, src.data_ptr(), n)
+    h = e.heal_stats()
+    assert h["failed_attempts"] >= 3 and h["retried_ok"] > 0
+    heal_ms = (h["first_reroute_ok_ns"] - h["fault_start_ns"]) / 1e6
+    assert 0 < heal_ms < 50.0, h
+    assert bytes_by_rail(e)[f"g0.rl{v}"] > 0
+    e.stop()

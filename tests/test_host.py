@@ -132,3 +132,34 @@ def test_hash128_matches_reference_construction():
     out = (C.c_uint64 * 2)()
     co.lib.so_hash128(b"kv/block0", 9, out)
     assert sp.hash128("kv/block0") == (out[0], out[1])
+
+
+def test_relay_rails_plan_as_spillover_tier():
+    """2-hop relay rails (executor "relay", via GPU K) are ordinary rails to the planner:
+    the direct SM pair first (tier 1), the relay pair behind it at tier 2 (the reference's
+    spillover tier, P = 3), like with like by position (orchestrator.cpp:59-67)."""
+    topo = fabrics.peer_fabric([0, 1], sm_rails=1, relay_via=[2])
+    e = sp.Engine(topo, json.dumps({}))
+    e.register_segment(sp.SegmentDescriptor("s", sp.Medium.DEVICE, "g0", [sp.BufferDesc(0, 1 << 20, 0x1000)]))
+    e.register_segment(sp.SegmentDescriptor("d", sp.Medium.DEVICE, "g1", [sp.BufferDesc(0, 1 << 20, 0x2000)]))
+    s, b = e.plan_candidates("s", "d")
+    ids = {e.rail_id(r): r for r in range(e.rail_count())}
+    # stream: 1 set, n locals, then per local: rail, n pairs, (remote, tier, affinity)...
+    n_loc = s[1]
+    locs, k = {}, 2
+    for _ in range(n_loc):
+        rail, npair = s[k], s[k + 1]
+        locs[rail] = [tuple(s[k + 2 + 3 * p:k + 5 + 3 * p]) for p in range(npair)]
+        k += 2 + 3 * npair
+    assert set(locs) == {ids["g0.nvl0"], ids["g0.rl2"]}
+    tiers = {r: {p[0]: p[1] for p in v} for r, v in locs.items()}
+    assert tiers[ids["g0.rl2"]][ids["g1.rl2"]] == 2
+    assert tiers[ids["g0.nvl0"]][ids["g1.nvl0"]] == 1
+
+
+def test_relay_rail_without_via_is_a_config_error():
+    topo = json.loads(fabrics.peer_fabric([0, 1], sm_rails=1, relay_via=[2]))
+    for r in topo["rails"]:
+        r.pop("via", None)
+    with pytest.raises(sp.ConfigError):
+        sp.Engine(json.dumps(topo), json.dumps({}))

@@ -5,7 +5,9 @@
             slices over cudaMemcpyAsync streams and vs one cudaMemcpyPeer of the whole GiB.
   elephant  the 8-GPU variant: 8 disjoint 1 GiB flows i -> (i+1) mod N, one engine per GPU.
   c4        broadcast S bytes GPU0 -> every other GPU (naive fan-out through GPU0's engine).
-  c5        c2 traffic; the direct SM rail goes DOWN mid-transfer: heal time and bytes.
+  c5        c2 traffic; the direct SM rail goes DOWN mid-transfer: heal time and bytes
+            (alternate: a copy-engine rail, or the relay rails of --relay-via).
+  --relay-via K [..]  add 2-hop relay rails through GPU K (tier 2, or --relay-affinity direct)
 
 Prints one JSON object per mode. Delivered bytes are checked with the device checksum.
 """
@@ -36,10 +38,14 @@ def buf(dev, n, seed=None):
 CE_GBS = 770.0  # declared bandwidth of copy-engine rails (--ce-gbs)
 
 
+RELAY = {"via": [], "affinity": "same_socket"}  # --relay-via / --relay-affinity
+
+
 def engine(dev, gpus, sm_rails, ce_rails, extra_cfg=None):
     cfg = {"resilience": {"degradation_ratio": 1e9}}
     cfg.update(extra_cfg or {})
-    e = sp.Engine(fabrics.peer_fabric(gpus, sm_rails=sm_rails, ce_rails=ce_rails, bw_ce=CE_GBS * 1e9),
+    e = sp.Engine(fabrics.peer_fabric(gpus, sm_rails=sm_rails, ce_rails=ce_rails, bw_ce=CE_GBS * 1e9,
+                                      relay_via=RELAY["via"], relay_affinity=RELAY["affinity"]),
                   json.dumps(cfg), dev)
     e.start()
     return e
@@ -265,7 +271,7 @@ def c4chain(args):
 def c5(args):
     n = args.size
     src, dst = buf(0, n, 91), buf(1, n)
-    e = engine(0, [0, 1], 1, max(1, args.ce_rails))
+    e = engine(0, [0, 1], 1, 0 if RELAY["via"] else max(1, args.ce_rails))
     reg(e, "src", 0, src)
     reg(e, "dst", 1, dst)
     b = e.allocate_batch()
@@ -328,7 +334,10 @@ def main():
     ap.add_argument("--fault-after-ms", type=float, default=0.3)
     ap.add_argument("--prof", action="store_true", help="c2: print scheduler-warp cycle counters")
     ap.add_argument("--ce-gbs", type=float, default=770.0, help="declared bandwidth of each copy-engine rail")
+    ap.add_argument("--relay-via", type=int, nargs="*", default=[], help="2-hop relay rails through these GPUs")
+    ap.add_argument("--relay-affinity", default="same_socket", help="relay rail tier (direct = tier 1)")
     args = ap.parse_args()
+    RELAY["via"], RELAY["affinity"] = args.relay_via, args.relay_affinity
     global CE_GBS
     CE_GBS = args.ce_gbs
     out = {"c2": c2, "elephant": elephant, "c4": c4, "c4chain": c4chain, "c5": c5}[args.mode](args)
