@@ -367,7 +367,10 @@ def nvlink_phase(sp, fabrics, args, rank, world, dev):
         if pc:
             b = ec.allocate_batch()
             ms = pc.run(b)
-            if ec.batch_status(b).state != sp.BatchState.COMPLETE:
+            st = ec.batch_status(b)
+            if st.state != sp.BatchState.COMPLETE:
+                print(f"rank {rank}: chain batch {st} counters {ec.counters()} heal {ec.heal_stats()}",
+                      file=sys.stderr, flush=True)
                 ms = 1e9
             ec.free_batch(b)
         ms = maxr(ms)

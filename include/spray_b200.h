@@ -210,11 +210,16 @@ int spray_prepare_transfers(spray_engine* e, const spray_transfer_request* reqs,
 int spray_run_prepared(spray_engine* e, uint64_t batch, spray_prepared* p, float* kernel_ms);
 void spray_prepared_free(spray_prepared* p);
 
-/* Multi-process peer segments: export a device allocation as a CUDA IPC handle (64 B) and
- * open a peer's handle in this process (the returned pointer can be registered as a
- * DEVICE segment on the peer's node). */
-int spray_ipc_export(int device, void* ptr, uint8_t handle_out[64]);
-int spray_ipc_open(int device, const uint8_t handle[64], void** ptr_out);
+/* Multi-process peer segments: export a device pointer as an IPC handle and open a peer's
+ * handle in this process (the returned pointer can be registered as a DEVICE segment on
+ * the peer's node). The handle is the CUDA IPC handle of the allocation that contains
+ * `ptr` (64 B) followed by ptr's byte offset inside it (8 B, little endian): pointers
+ * handed out by sub-allocating pools (e.g. PyTorch's caching allocator) map to the same
+ * bytes in the importing process. spray_ipc_close takes the pointer spray_ipc_open
+ * returned. */
+#define SPRAY_IPC_HANDLE_BYTES 72
+int spray_ipc_export(int device, void* ptr, uint8_t handle_out[SPRAY_IPC_HANDLE_BYTES]);
+int spray_ipc_open(int device, const uint8_t handle[SPRAY_IPC_HANDLE_BYTES], void** ptr_out);
 int spray_ipc_close(void* ptr);
 
 /* Host planning only (no GPU work): the candidate stream of the route the engine would

@@ -403,24 +403,70 @@ int spray_rr_copy(int device, const uint64_t* src, const uint64_t* dst, const ui
   });
 }
 
-int spray_ipc_export(int device, void* ptr, uint8_t handle_out[64]) {
+// The allocation base of a device pointer: cuMemGetAddressRange through the runtime's
+// driver entry point (no link-time dependency on libcuda).
+static uint64_t alloc_base(void* ptr) {
+  using Fn = int (*)(unsigned long long*, size_t*, unsigned long long);
+  static Fn fn = nullptr;
+  if (!fn) {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    CK(cudaGetDriverEntryPoint("cuMemGetAddressRange", &f, cudaEnableDefault, &q));
+    if (!f || q != cudaDriverEntryPointSuccess) throw EngineError("cuMemGetAddressRange unavailable");
+    fn = reinterpret_cast<Fn>(f);
+  }
+  unsigned long long base = 0;
+  size_t size = 0;
+  if (fn(&base, &size, reinterpret_cast<unsigned long long>(ptr)) != 0)
+    throw InvalidRangeError("ipc export: pointer is not inside a device allocation");
+  return base;
+}
+
+static std::mutex g_ipc_mu;
+static std::map<uint64_t, std::pair<uint64_t, int>> g_ipc_open;  // returned ptr -> (mapped base, refs)
+
+int spray_ipc_export(int device, void* ptr, uint8_t handle_out[SPRAY_IPC_HANDLE_BYTES]) {
   return guard([&] {
     CK(cudaSetDevice(device));
     cudaIpcMemHandle_t h;
     CK(cudaIpcGetMemHandle(&h, ptr));
     static_assert(sizeof(h) == 64, "ipc handle is 64 B");
+    const uint64_t off = reinterpret_cast<uint64_t>(ptr) - alloc_base(ptr);
     std::memcpy(handle_out, &h, 64);
+    std::memcpy(handle_out + 64, &off, 8);
   });
 }
-int spray_ipc_open(int device, const uint8_t handle[64], void** ptr_out) {
+int spray_ipc_open(int device, const uint8_t handle[SPRAY_IPC_HANDLE_BYTES], void** ptr_out) {
   return guard([&] {
     CK(cudaSetDevice(device));
     cudaIpcMemHandle_t h;
+    uint64_t off = 0;
     std::memcpy(&h, handle, 64);
-    CK(cudaIpcOpenMemHandle(ptr_out, h, cudaIpcMemLazyEnablePeerAccess));
+    std::memcpy(&off, handle + 64, 8);
+    void* base = nullptr;
+    CK(cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess));
+    const uint64_t p = reinterpret_cast<uint64_t>(base) + off;
+    std::lock_guard<std::mutex> lk(g_ipc_mu);
+    auto& e = g_ipc_open[p];
+    e.first = reinterpret_cast<uint64_t>(base);
+    ++e.second;
+    *ptr_out = reinterpret_cast<void*>(p);
   });
 }
-int spray_ipc_close(void* ptr) { return guard([&] { CK(cudaIpcCloseMemHandle(ptr)); }); }
+int spray_ipc_close(void* ptr) {
+  return guard([&] {
+    uint64_t base = reinterpret_cast<uint64_t>(ptr);
+    {
+      std::lock_guard<std::mutex> lk(g_ipc_mu);
+      auto it = g_ipc_open.find(base);
+      if (it != g_ipc_open.end()) {
+        base = it->second.first;
+        if (--it->second.second == 0) g_ipc_open.erase(it);
+      }
+    }
+    CK(cudaIpcCloseMemHandle(reinterpret_cast<void*>(base)));
+  });
+}
 
 }  // extern "C"
 

@@ -225,7 +225,8 @@ struct GateDev {
 // kernel running on K's SMs moves it to the destination and does the chunk's completion
 // accounting in this engine's counters (peer atomics), so to the scheduler a relay chunk
 // completes like any other chunk. Tickets restart at 0 every launch (the prologue clears
-// `tail` and `seq`); descriptor stamps carry the launch generation.
+// `tail` and `seq`, the host clears `head` on K's stream); descriptor stamps carry the
+// launch generation.
 constexpr int kMaxRelays = 8;
 struct RelayDesc {  // 32 B, in K's HBM: written by the hop-1 worker, read by the forwarder
   uint64_t dst;
@@ -238,6 +239,7 @@ struct RelayDev {
   uint32_t* exit_gen;           // K's HBM: the engine writes its launch generation on exit
   uint32_t* seq;                // this GPU's HBM: per-slot free round (forwarder -> workers)
   unsigned long long* tail;     // this GPU's HBM: hop-1 ticket counter (workers)
+  unsigned long long* head;     // K's HBM: hop-2 ticket counter (forwarder warps)
   uint32_t n_slots, via;        // power of two; relay GPU ordinal
 };
 

@@ -13,7 +13,7 @@ namespace spray_launch {
 size_t engine_smem_bytes();
 cudaError_t launch_engine(const spray_dev::EngineDev& E, int grid, int block, cudaStream_t st);
 cudaError_t launch_epoch(uint64_t* out, cudaStream_t st);
-cudaError_t launch_relay_forward(const spray_dev::EngineDev& E, uint32_t r, cudaStream_t st);
+cudaError_t launch_relay_forward(const spray_dev::EngineDev& E, uint32_t r, int grid, cudaStream_t st);
 }  // namespace spray_launch
 
 namespace spray {
@@ -457,7 +457,7 @@ void Engine::setup_relay(uint32_t idx, int via) {
   RelayHost h;
   h.via = via;
   CK(cudaStreamCreateWithFlags(&h.stream, cudaStreamNonBlocking));
-  constexpr uint32_t kSlots = 1024;  // a multiple of the forwarder's 512 warps
+  constexpr uint32_t kSlots = 2048;  // power of two
   RelayDev R{};
   R.n_slots = kSlots;
   R.via = static_cast<uint32_t>(via);
@@ -471,6 +471,7 @@ void Engine::setup_relay(uint32_t idx, int via) {
   R.staging = static_cast<uint8_t*>(on_via(size_t(kSlots) << E_.chunk_shift));
   R.desc = static_cast<RelayDesc*>(on_via(sizeof(RelayDesc) * kSlots));
   R.exit_gen = static_cast<uint32_t*>(on_via(sizeof(uint32_t)));
+  R.head = static_cast<unsigned long long*>(on_via(sizeof(unsigned long long)));
   CK(cudaSetDevice(device_));
   R.seq = static_cast<uint32_t*>(nullptr);
   void* p = nullptr;
@@ -587,7 +588,10 @@ void Engine::launch() {
   CK(spray_launch::launch_engine(E_, grid, opts_.block, stream_));
   for (uint32_t r = 0; r < relays_.size(); ++r) {  // hop 2 on each relay GPU
     CK(cudaSetDevice(relays_[r].via));
-    CK(spray_launch::launch_relay_forward(E_, r, relays_[r].stream));
+    int sms = 0;
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, relays_[r].via));
+    CK(cudaMemsetAsync(E_.relays[r].head, 0, sizeof(unsigned long long), relays_[r].stream));
+    CK(spray_launch::launch_relay_forward(E_, r, sms, relays_[r].stream));
   }
   if (!relays_.empty()) CK(cudaSetDevice(device_));
 }

@@ -521,14 +521,17 @@ def host_free(p: int):
     _check(lib.spray_host_free(p))
 
 
+IPC_HANDLE_BYTES = 72  # SPRAY_IPC_HANDLE_BYTES: CUDA IPC handle + offset inside the allocation
+
+
 def ipc_export(device: int, ptr: int) -> bytes:
-    buf = (C.c_uint8 * 64)()
+    buf = (C.c_uint8 * IPC_HANDLE_BYTES)()
     _check(lib.spray_ipc_export(device, ptr, buf))
     return bytes(buf)
 
 
 def ipc_open(device: int, handle: bytes) -> int:
-    buf = (C.c_uint8 * 64).from_buffer_copy(handle)
+    buf = (C.c_uint8 * IPC_HANDLE_BYTES).from_buffer_copy(handle)
     p = C.c_void_p()
     _check(lib.spray_ipc_open(device, buf, C.byref(p)))
     return p.value

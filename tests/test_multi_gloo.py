@@ -28,7 +28,7 @@ def _worker(rank, world, port, q):
     e.register_segment(sp.SegmentDescriptor("hbm", sp.Medium.DEVICE, f"g{rank}", [sp.BufferDesc(0, 1 << 20, 0x1000)]))
     e.register_segment(sp.SegmentDescriptor("host", sp.Medium.HOST, f"g{rank}", [sp.BufferDesc(0, 1 << 20, 0x2000)]))
     stream, backend = e.plan_candidates("hbm", "host")
-    handle = bytes([rank]) * 64  # stands in for a cudaIpcMemHandle exported by spray_ipc_export
+    handle = bytes([rank]) * sp.IPC_HANDLE_BYTES  # stands in for a handle exported by spray_ipc_export
     shards = [None] * world
     dist.all_gather_object(shards, (first, last, stream.tolist(), backend, handle))
     peer = sharding.flow_peer(rank, world)
@@ -61,4 +61,9 @@ def test_two_rank_sharding_and_handle_exchange():
     assert sorted(covered) == list(range(4096))
     assert [r[2] for r in res] == [1, 0]
     assert all(r[3] == 2.0 for r in res)
-    assert shards[1][4] == bytes([1]) * 64
+    assert shards[1][4] == bytes([1]) * sp_handle_bytes()
+
+
+def sp_handle_bytes():
+    import paper_2604_00368_b200 as sp
+    return sp.IPC_HANDLE_BYTES
