@@ -37,7 +37,7 @@ def _worker(rank, world, port, n, q):
         pad = torch.zeros(4096 + 512 * rank, dtype=torch.uint8, device=f"cuda:{rank}")  # noqa: F841
         small = torch.zeros(64 << 10, dtype=torch.uint8, device=f"cuda:{rank}")  # noqa: F841
         buf = torch.zeros(n, dtype=torch.uint8, device=f"cuda:{rank}")  # inside a pooled block
-        e = sp.Engine(fabrics.peer_fabric([rank, (rank + 1) % world]), json.dumps({}), rank)
+        e = sp.Engine(fabrics.peer_fabric([rank, (rank + 1) % world]), json.dumps({"b200": {"chunk_bytes": 65536}}), rank)
         e.start()
         cb = e.chunk_bytes()
         flags = torch.zeros(n // cb, dtype=torch.int32, device=f"cuda:{rank}")

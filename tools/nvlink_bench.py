@@ -43,6 +43,8 @@ RELAY = {"via": [], "affinity": "same_socket"}  # --relay-via / --relay-affinity
 
 def engine(dev, gpus, sm_rails, ce_rails, extra_cfg=None):
     cfg = {"resilience": {"degradation_ratio": 1e9}}
+    if RELAY.get("chunk"):
+        cfg["b200"] = {"chunk_bytes": RELAY["chunk"]}
     cfg.update(extra_cfg or {})
     e = sp.Engine(fabrics.peer_fabric(gpus, sm_rails=sm_rails, ce_rails=ce_rails, bw_ce=CE_GBS * 1e9,
                                       relay_via=RELAY["via"], relay_affinity=RELAY["affinity"]),
@@ -336,8 +338,10 @@ def main():
     ap.add_argument("--ce-gbs", type=float, default=770.0, help="declared bandwidth of each copy-engine rail")
     ap.add_argument("--relay-via", type=int, nargs="*", default=[], help="2-hop relay rails through these GPUs")
     ap.add_argument("--relay-affinity", default="same_socket", help="relay rail tier (direct = tier 1)")
+    ap.add_argument("--chunk-kib", type=int, default=0, help="b200.chunk_bytes (SM work granule), KiB")
     args = ap.parse_args()
     RELAY["via"], RELAY["affinity"] = args.relay_via, args.relay_affinity
+    RELAY["chunk"] = args.chunk_kib << 10 if args.chunk_kib else 0
     global CE_GBS
     CE_GBS = args.ce_gbs
     out = {"c2": c2, "elephant": elephant, "c4": c4, "c4chain": c4chain, "c5": c5}[args.mode](args)
