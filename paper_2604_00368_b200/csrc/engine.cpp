@@ -1240,7 +1240,7 @@ void Engine::ce_proxy_loop(int k) {
   // contiguous run), else one cudaMemcpy2DAsync (rows = slices; the copy engines move
   // pitch-linear rows natively). Completions stay per order, reported when the group's
   // event fires.
-  constexpr int kMaxGroup = 64;
+  constexpr int kMaxGroup = 1024;  // orders taken per pass (one completion event per pass)
   struct Run {
     uint64_t src = 0, dst = 0, len = 0, spitch = 0, dpitch = 0, rows = 0;
   } run;

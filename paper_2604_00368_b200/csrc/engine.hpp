@@ -33,7 +33,7 @@ struct EngineOptions {
   // B200 execution parameters ("b200" section of the config document)
   int grid = 0;                 // 0 = one CTA per SM
   int block = 256;
-  uint64_t chunk_bytes = 128 << 10;
+  uint64_t chunk_bytes = 32 << 10;  // finer granules shorten the tail: C2 1 GiB 619 -> 653 GB/s (32 KiB), flat at 4 GiB
   uint64_t idle_exit_ns = 20'000'000;
   uint32_t slice_capacity = 1u << 17;
   uint64_t work_capacity = 1ull << 21;

@@ -19,9 +19,10 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--fabric", default="kv", choices=["kv", "hbm"])
     ap.add_argument("--reps", type=int, default=300)
+    ap.add_argument("--chunk-kib", type=int, default=64)
     a = ap.parse_args()
     dev = 0
-    cfg = {"resilience": {"degradation_ratio": 1e9}, "b200": {"chunk_bytes": 65536}}
+    cfg = {"resilience": {"degradation_ratio": 1e9}, "b200": {"chunk_bytes": a.chunk_kib << 10}}
     if a.fabric == "kv":
         e = sp.Engine(fabrics.kv_offload(dev), json.dumps(cfg), dev)
     else:
@@ -38,7 +39,7 @@ def main():
         dst = torch.zeros(n, dtype=torch.uint8, device="cuda:0")
         e.register_segment(sp.SegmentDescriptor("s", sp.Medium.DEVICE, "a", [sp.BufferDesc(0, n, hbm.data_ptr())]))
         e.register_segment(sp.SegmentDescriptor("d", sp.Medium.DEVICE, "b", [sp.BufferDesc(0, n, dst.data_ptr())]))
-    out = {"fabric": a.fabric}
+    out = {"fabric": a.fabric, "chunk_kib": a.chunk_kib}
     for nint, blk in ((1, 4096), (1, 65536), (8, 65536), (64, 65536), (1, 4 << 20), (256, 65536)):
         reqs = sp.Requests([sp.TransferRequest("s", i * blk, "d", i * blk, blk) for i in range(nint)])
         lat, sub = [], []

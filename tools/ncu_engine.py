@@ -24,7 +24,7 @@ ap.add_argument("--blocks", type=int, default=4096)
 args = ap.parse_args()
 
 blk, nb = 64 << 10, args.blocks
-e = sp.Engine(fabrics.kv_offload(0), json.dumps({"resilience": {"degradation_ratio": 1e9}}), 0)
+e = sp.Engine(fabrics.kv_offload(0), json.dumps({"resilience": {"degradation_ratio": 1e9}, "b200": {"chunk_bytes": 65536}}), 0)
 e.start()
 hbm = torch.empty(blk * nb, dtype=torch.uint8, device="cuda:0")
 hbm2 = torch.zeros(blk * nb, dtype=torch.uint8, device="cuda:0")
