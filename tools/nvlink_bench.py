@@ -7,6 +7,8 @@
   c4        broadcast S bytes GPU0 -> every other GPU (naive fan-out through GPU0's engine).
   c5        c2 traffic; the direct SM rail goes DOWN mid-transfer: heal time and bytes
             (alternate: a copy-engine rail, or the relay rails of --relay-via).
+  congest   c2 over several rails with one DEGRADEd (injected congestion): telemetry vs
+            round-robin policy.
   --relay-via K [..]  add 2-hop relay rails through GPU K (tier 2, or --relay-affinity direct)
 
 Prints one JSON object per mode. Delivered bytes are checked with the device checksum.
@@ -326,9 +328,35 @@ def c5(args):
     return {"mode": "c5", "bytes": n, "complete_and_bit_exact": bool(ok), "heal": heal, "rails": stats}
 
 
+def congest(args):
+    """Injected congestion on C2: the flow sprays over the direct SM rail(s) and any
+    --relay-via rails (tier 1); rail --congest-rail is DEGRADEd to --factor of its
+    bandwidth for the whole run (sim_backend.cpp:171-181 semantics on the real fabric).
+    Telemetry spraying vs the state-blind round-robin policy (a25), same rails."""
+    n = args.size
+    src, dst = buf(0, n, 61), buf(1, n)
+    out = {"mode": "congest", "bytes": n, "congested": args.congest_rail, "factor": args.factor}
+    for pol in ("telemetry", "rr"):
+        e = engine(0, [0, 1], args.sm_rails, args.ce_rails, {"scheduler": {"policy": pol}})
+        reg(e, "src", 0, src)
+        reg(e, "dst", 1, dst)
+        now = e.now_ns()
+        e.inject_fault(args.congest_rail, sp.FaultEffect.DEGRADE, now, now + 10 ** 13, args.factor)
+        best, mean = timed_prepared(e, [sp.TransferRequest("src", 0, "dst", 0, n)], args.reps)
+        assert sp.checksum(1, dst.data_ptr(), n) == sp.checksum(0, src.data_ptr(), n)
+        stats = [e.rail_stats(r) for r in range(e.rail_count())]
+        tot = sum(x.bytes_ok for x in stats) or 1
+        out[pol] = {"gbs": round(n / (mean * 1e-3) / 1e9, 2),
+                    "share": {x.rail_id: round(x.bytes_ok / tot, 3) for x in stats if x.bytes_ok}}
+        e.stop()
+        dst.zero_()
+    out["telemetry_over_rr"] = round(out["telemetry"]["gbs"] / out["rr"]["gbs"], 3)
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("mode", choices=["c2", "elephant", "c4", "c4chain", "c5"])
+    ap.add_argument("mode", choices=["c2", "elephant", "c4", "c4chain", "c5", "congest"])
     ap.add_argument("--size", type=int, default=GiB)
     ap.add_argument("--sm-rails", type=int, default=1)
     ap.add_argument("--ce-rails", type=int, default=0)
@@ -339,12 +367,14 @@ def main():
     ap.add_argument("--relay-via", type=int, nargs="*", default=[], help="2-hop relay rails through these GPUs")
     ap.add_argument("--relay-affinity", default="same_socket", help="relay rail tier (direct = tier 1)")
     ap.add_argument("--chunk-kib", type=int, default=0, help="b200.chunk_bytes (SM work granule), KiB")
+    ap.add_argument("--congest-rail", default="g0.nvl0", help="congest: the DEGRADEd rail")
+    ap.add_argument("--factor", type=float, default=0.25, help="congest: bandwidth factor of the DEGRADEd rail")
     args = ap.parse_args()
     RELAY["via"], RELAY["affinity"] = args.relay_via, args.relay_affinity
     RELAY["chunk"] = args.chunk_kib << 10 if args.chunk_kib else 0
     global CE_GBS
     CE_GBS = args.ce_gbs
-    out = {"c2": c2, "elephant": elephant, "c4": c4, "c4chain": c4chain, "c5": c5}[args.mode](args)
+    out = {"c2": c2, "elephant": elephant, "c4": c4, "c4chain": c4chain, "c5": c5, "congest": congest}[args.mode](args)
     print(json.dumps(out), flush=True)
     os._exit(0)
 
