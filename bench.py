@@ -342,8 +342,8 @@ def nvlink_phase(sp, fabrics, args, rank, world, dev):
         sp.fill_splitmix(dev, w.data_ptr(), nb_, 4242)
     else:
         w.zero_()
-    chain_cfg = json.dumps({"resilience": {"degradation_ratio": 1e9}})
-    cb = 65536
+    cb = 65536  # the gate granule: b200.chunk_bytes of the chain engines, one flag per granule
+    chain_cfg = json.dumps({"resilience": {"degradation_ratio": 1e9}, "b200": {"chunk_bytes": cb}})
     flags = torch.zeros(nb_ // cb, dtype=torch.int32, device=f"cuda:{dev}")
     hs = gather((sp.ipc_export(dev, w.data_ptr()), sp.ipc_export(dev, flags.data_ptr())))
     ec, pc = None, None

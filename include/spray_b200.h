@@ -222,6 +222,17 @@ int spray_ipc_export(int device, void* ptr, uint8_t handle_out[SPRAY_IPC_HANDLE_
 int spray_ipc_open(int device, const uint8_t handle[SPRAY_IPC_HANDLE_BYTES], void** ptr_out);
 int spray_ipc_close(void* ptr);
 
+/* GlobalLoadBoard (scheduler.hpp:66-90, scheduler.cpp:63-79): engines publish their
+ * per-rail queued bytes into slots of a shared board every `period_ns` (control phase,
+ * engine.cpp:1090-1093), and blend the board's fresh entries (heartbeat within 3 periods)
+ * into their effective queue with scheduler.diffusion_weight. The board is caller-owned,
+ * zeroed host memory of spray_board_bytes(n_slots) bytes (pinned or pageable: the engine
+ * maps it; share it across processes with shared memory); `slot` is this engine's
+ * instance. Heartbeats are GPU global-timer nanoseconds, common to the GPUs of a host.
+ * Attach while no batch is in flight. */
+size_t spray_board_bytes(uint32_t n_slots);
+int spray_engine_attach_board(spray_engine* e, void* board, uint32_t n_slots, uint32_t slot, uint64_t period_ns);
+
 /* Host planning only (no GPU work): the candidate stream of the route the engine would
  * use for src -> dst (orchestrator.cpp:98-245 + 39-81), and the backend serving it. */
 int spray_plan_candidates(spray_engine* e, const char* src_segment, const char* dst_segment,
@@ -247,11 +258,15 @@ int spray_plan_candidates(spray_engine* e, const char* src_segment, const char* 
  *                                      elapsed go to PROBING       (resilience.cpp:220-244)
  *   PROBE_DONE(rail, len, status, now=now_ns)  release(rail,len); observe_probe(rail,
  *                                      status, now)                (resilience.cpp:191-212)
+ *   BOARD(rail, len=(int64) global queued bytes, now=now_ns)  the load board's
+ *                                      global_queued(rail) seen by every later
+ *                                      effective_queued(rail) until the next BOARD event
+ *                                      of the rail (scheduler.cpp:63-79, 108-114, 249-254)
  */
 enum spray_trace_kind {
   SPRAY_EV_DECIDE = 1, SPRAY_EV_COMPLETE = 2, SPRAY_EV_CHARGE = 3, SPRAY_EV_RELEASE = 4,
   SPRAY_EV_HEALTH = 5, SPRAY_EV_RESET = 6, SPRAY_EV_RESET_RAIL = 7, SPRAY_EV_EXPECT_HEALTH = 8,
-  SPRAY_EV_DUE_PROBES = 9, SPRAY_EV_PROBE_DONE = 10
+  SPRAY_EV_DUE_PROBES = 9, SPRAY_EV_PROBE_DONE = 10, SPRAY_EV_BOARD = 11
 };
 #define SPRAY_EVF_MODEL 0x1u
 #define SPRAY_EVF_CANCELLED 0x2u
@@ -292,6 +307,8 @@ typedef struct spray_sched_config {
   double beta0_init_s;
   double beta1_init;
   double feedback_clamp;
+  double diffusion_weight;   /* omega (scheduler.hpp:51): blend of the global load board;
+                                0 disables it, as does the absence of a board */
 } spray_sched_config;
 
 /* Resilience constants (spray::ResilienceConfig, resilience.hpp:17-31). */

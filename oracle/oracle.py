@@ -29,7 +29,7 @@ DECISION_DTYPE = np.dtype([
 assert EVENT_DTYPE.itemsize == 64 and DECISION_DTYPE.itemsize == 32
 
 EV_DECIDE, EV_COMPLETE, EV_CHARGE, EV_RELEASE, EV_HEALTH, EV_RESET, EV_RESET_RAIL, EV_EXPECT = range(1, 9)
-EV_DUE_PROBES, EV_PROBE_DONE = 9, 10
+EV_DUE_PROBES, EV_PROBE_DONE, EV_BOARD = 9, 10, 11
 EVF_MODEL, EVF_CANCELLED = 1, 2
 NO_RAIL = 0xFFFFFFFF
 
@@ -39,7 +39,7 @@ class SchedConfig(C.Structure):
                 ("policy", C.c_int32), ("tolerance", C.c_double), ("penalty", C.c_double * 3),
                 ("ewma_alpha", C.c_double), ("reset_interval_ns", C.c_uint64),
                 ("beta0_init_s", C.c_double), ("beta1_init", C.c_double),
-                ("feedback_clamp", C.c_double)]
+                ("feedback_clamp", C.c_double), ("diffusion_weight", C.c_double)]
 
 
 class ResConfig(C.Structure):
@@ -61,7 +61,7 @@ class BackendCaps(C.Structure):
 
 def sched_config(policy=0, tolerance=0.05, penalties=(1.0, 3.0, 0.0), alpha=0.2,
                  reset_interval_ns=30_000_000_000, min_slice=65536, max_slices=4096,
-                 beta0=0.0, beta1=1.0, clamp=5.0) -> SchedConfig:
+                 beta0=0.0, beta1=1.0, clamp=5.0, omega=0.0) -> SchedConfig:
     """Defaults of spray::SchedulerConfig (scheduler.hpp:44-58)."""
     c = SchedConfig()
     c.min_slice_size, c.max_slices_per_transfer, c.policy = min_slice, max_slices, policy
@@ -70,6 +70,7 @@ def sched_config(policy=0, tolerance=0.05, penalties=(1.0, 3.0, 0.0), alpha=0.2,
         c.penalty[i] = penalties[i] if penalties[i] is not None else 0.0
     c.ewma_alpha, c.reset_interval_ns = alpha, reset_interval_ns
     c.beta0_init_s, c.beta1_init, c.feedback_clamp = beta0, beta1, clamp
+    c.diffusion_weight = omega
     return c
 
 

@@ -47,6 +47,7 @@ SchedulerConfig to_ref(const spray_sched_config* c) {
   s.beta0_init_s = c->beta0_init_s;
   s.beta1_init = c->beta1_init;
   s.feedback_clamp = c->feedback_clamp;
+  s.diffusion_weight = c->diffusion_weight;
   return s;
 }
 
@@ -229,7 +230,13 @@ int ref_replay(const char* topo, const spray_sched_config* sc, const spray_resil
                int64_t* queued_out, double* beta_out, int32_t* health_out) {
   try {
     TopologyGraph g = load_topology(topo);
-    SliceScheduler sched(&g, to_ref(sc));
+    // omega > 0: a board is attached (trace semantics, spray_b200.h BOARD event). A
+    // BOARD(rail, G) event makes global_queued(rail) == G exactly: this instance
+    // publishes its own queues (publish_to_board, which also sets the time hint) and an
+    // external instance publishes the remainder G - own.
+    GlobalLoadBoard board(10 * kMilli);
+    const bool with_board = sc->diffusion_weight > 0.0;
+    SliceScheduler sched(&g, to_ref(sc), with_board ? &board : nullptr, "engine0");
     Telemetry tel(&g, 10 * kMilli, false);
     ResilienceManager res(&g, &sched, &tel, to_ref(rc));
     auto sets = parse_sets(cand_stream, cand_len);
@@ -277,6 +284,12 @@ int ref_replay(const char* topo, const spray_sched_config* sc, const spray_resil
           if (static_cast<uint32_t>(sched.health(e.rail)) != e.flags) ++bad;
           break;
         case SPRAY_EV_DUE_PROBES: (void)res.due_probes(e.t_ns); break;
+        case SPRAY_EV_BOARD: {
+          if (!with_board) break;
+          sched.publish_to_board(e.now_ns);
+          board.publish("ext", e.rail, static_cast<int64_t>(e.len) - sched.queued_bytes(e.rail), e.now_ns);
+          break;
+        }
         case SPRAY_EV_PROBE_DONE: {
           const int status = static_cast<int>((e.flags >> 8) & 0xff);
           sched.release(e.rail, e.len);

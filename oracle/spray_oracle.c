@@ -97,6 +97,7 @@ int so_sched_config_validate(const spray_sched_config* c) {
   if (c->max_slices_per_transfer == 0) return -1;
   if (!(c->tolerance > 0.0)) return -1;
   if (c->ewma_alpha <= 0.0 || c->ewma_alpha > 1.0) return -1;
+  if (c->diffusion_weight < 0.0 || c->diffusion_weight > 1.0) return -1; /* scheduler.cpp:39-40 */
   double prev = 0.0;
   for (int t = 1; t <= 3; ++t) {
     if (!pen_ok(c, t)) {
@@ -126,10 +127,20 @@ void so_sched_init(so_sched* s, const spray_sched_config* sc, const spray_resili
   }
 }
 
-/* scheduler.cpp:108-122 (diffusion weight 0: effective queue = local queue) */
+/* scheduler.cpp:108-114 effective_queued: the local queue, blended with the board's
+ * global view (the last BOARD event of the rail; 0 before the first) when omega > 0.
+ * Trace semantics: omega > 0 means a board is attached. */
+static double so_effective_queued(const so_sched* s, uint32_t rail) {
+  const double local = (double)s->rails[rail].queued;
+  if (!(s->cfg.diffusion_weight > 0.0)) return local;  /* omega > 0 <=> a board is attached */
+  const double global = (double)s->board_g[rail];
+  return (1.0 - s->cfg.diffusion_weight) * local + s->cfg.diffusion_weight * global;
+}
+
+/* scheduler.cpp:116-122 */
 double so_predict_completion_s(const so_sched* s, uint32_t rail, uint64_t len) {
   const so_rail* st = &s->rails[rail];
-  const double a = (double)st->queued;
+  const double a = so_effective_queued(s, rail);
   return st->beta0 + st->beta1 * ((a + (double)len) / st->bandwidth);
 }
 
@@ -162,7 +173,7 @@ int so_choose_rail(so_sched* s, uint64_t len, uint64_t offset, const so_cset* cs
     if (!pen_ok(&s->cfg, p->tier)) continue;
     const double penalty = s->cfg.penalty[p->tier - 1];
     const so_rail* st = &s->rails[c->local];
-    const double x = ((double)st->queued + (double)len) / st->bandwidth;
+    const double x = (so_effective_queued(s, c->local) + (double)len) / st->bandwidth;
     const double predicted = st->beta0 + st->beta1 * x;
     el[ne].local = c->local;
     el[ne].remote = p->remote;
@@ -406,6 +417,7 @@ int so_replay(so_sched* s, const so_cset* sets, uint32_t n_sets, const spray_tra
         if (s->rails[e->rail].health != (int)e->flags) ++bad;
         break;
       case SPRAY_EV_DUE_PROBES: so_due_probes(s, e->t_ns); break;
+      case SPRAY_EV_BOARD: s->board_g[e->rail] = (int64_t)e->len; break;
       case SPRAY_EV_PROBE_DONE:
         so_release(s, e->rail, e->len);
         so_observe_probe(s, e->rail, (int)((e->flags >> 8) & 0xff), e->now_ns);

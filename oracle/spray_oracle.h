@@ -74,6 +74,7 @@ typedef struct so_sched {
   uint32_t id_rank[SO_MAX_RAILS];
   uint64_t rr_cursor;
   uint64_t exclusions;
+  int64_t board_g[SO_MAX_RAILS];  /* GlobalLoadBoard::global_queued(rail) (BOARD events) */
 } so_sched;
 
 void so_sched_init(so_sched* s, const spray_sched_config* sc, const spray_resilience_config* rc,

@@ -19,7 +19,8 @@ class SchedConfig(C.Structure):
     _fields_ = [("min_slice_size", C.c_uint64), ("max_slices_per_transfer", C.c_uint32),
                 ("policy", C.c_int32), ("tolerance", C.c_double), ("penalty", C.c_double * 3),
                 ("ewma_alpha", C.c_double), ("reset_interval_ns", C.c_uint64),
-                ("beta0_init_s", C.c_double), ("beta1_init", C.c_double), ("feedback_clamp", C.c_double)]
+                ("beta0_init_s", C.c_double), ("beta1_init", C.c_double), ("feedback_clamp", C.c_double),
+                ("diffusion_weight", C.c_double)]
 
 
 class ResConfig(C.Structure):
@@ -107,6 +108,8 @@ _SIGS = {
     "spray_heal_stats": (C.c_int, [P, U64P, U64P, U64P, U64P]),
     "spray_gate_segment": (C.c_int, [P, C.c_char_p, C.c_int, P]),
     "spray_engine_chunk_bytes": (C.c_int, [P, U64P]),
+    "spray_board_bytes": (C.c_size_t, [C.c_uint32]),
+    "spray_engine_attach_board": (C.c_int, [P, P, C.c_uint32, C.c_uint32, C.c_uint64]),
     "spray_telemetry_csv": (C.c_int, [P, C.c_char_p, C.c_size_t, SZP]),
     "spray_engine_debug": (C.c_int, [P, U64P, C.c_size_t]),
     "spray_trace_enable": (C.c_int, [P, C.c_size_t]),

@@ -167,6 +167,10 @@ int spray_telemetry_csv(spray_engine* e, char* buf, size_t cap, size_t* len) {
   });
 }
 
+size_t spray_board_bytes(uint32_t n_slots) { return spray::board_bytes(n_slots); }
+int spray_engine_attach_board(spray_engine* e, void* board, uint32_t n_slots, uint32_t slot, uint64_t period_ns) {
+  return guard([&] { e->eng->attach_board(board, n_slots, slot, period_ns); });
+}
 int spray_engine_chunk_bytes(spray_engine* e, uint64_t* out) {
   return guard([&] { *out = e->eng->chunk_bytes(); });
 }
@@ -320,6 +324,7 @@ int spray_replay_device(int device, const spray_sched_config* sc, const spray_re
       E.beta0_init = sc->beta0_init_s;
       E.beta1_init = sc->beta1_init;
       E.clamp = sc->feedback_clamp;
+      E.omega = sc->diffusion_weight;  // trace semantics: omega > 0 <=> a board is attached
       E.reset_interval = sc->reset_interval_ns;
       E.policy = static_cast<uint32_t>(sc->policy);
       E.failure_threshold = rc->failure_threshold;

@@ -243,6 +243,14 @@ struct RelayDev {
   uint32_t n_slots, via;        // power of two; relay GPU ordinal
 };
 
+// GlobalLoadBoard slot (scheduler.hpp:66-90) in caller-owned shared host memory: one per
+// engine instance; `heartbeat` = GPU global timer at the slot's last publish.
+struct BoardSlot {
+  uint64_t heartbeat;
+  uint64_t pad_;
+  int64_t queued[kMaxRails];
+};
+
 // Everything the kernel needs, passed by value.
 struct EngineDev {
   Control* ctl;                      // mapped host
@@ -295,6 +303,11 @@ struct EngineDev {
   RelayDev relays[kMaxRelays];                 // relay rails (RailDesc::ce_index = relay index)
   uint32_t n_relays;
   uint32_t launch_gen;                         // bumped by the host on every launch
+  double omega;                                // diffusion weight (0 unless a board is attached)
+  BoardSlot* board;                            // mapped host: the load board (null = none)
+  int64_t* board_hbm;                          // HBM: the adopted global view, kept across launches
+  uint32_t board_slots, board_slot;
+  uint64_t board_period;                       // publish period, ns (staleness = 3 periods)
 };
 
 // scalars persisted in EngineDev::persist between launches

@@ -39,6 +39,7 @@ void default_sched_config(spray_sched_config* c) {  // scheduler.hpp:44-58
   c->beta0_init_s = 0.0;
   c->beta1_init = 1.0;
   c->feedback_clamp = 5.0;
+  c->diffusion_weight = 0.0;  // scheduler.hpp:51
 }
 
 void default_resilience_config(spray_resilience_config* c) {  // resilience.hpp:17-28
@@ -71,7 +72,6 @@ static void validate(const spray_sched_config& c, double omega) {
   if (!(c.tolerance > 0.0)) throw ConfigError("tolerance must be > 0");
   if (c.ewma_alpha <= 0.0 || c.ewma_alpha > 1.0) throw ConfigError("alpha must be in (0, 1]");
   if (omega < 0.0 || omega > 1.0) throw ConfigError("diffusion weight must be in [0, 1]");
-  if (omega != 0.0) throw ConfigError("diffusion weight > 0 (global load board) is not part of this data plane");
   double prev = 0.0;
   for (int t = 0; t < 3; ++t) {
     if (!(c.penalty[t] > 0.0)) {
@@ -139,6 +139,7 @@ EngineOptions engine_options_from_json(const std::string& text) {
       if (s.contains("reset_interval_ms"))
         c.reset_interval_ns = static_cast<uint64_t>(s.at("reset_interval_ms").as_number() * 1e6);
       eo.diffusion_weight = s.number_or("diffusion_weight", 0.0);
+      c.diffusion_weight = eo.diffusion_weight;
       if (s.contains("policy")) {
         const std::string p = s.at("policy").as_string();
         if (p == "telemetry") c.policy = SPRAY_POLICY_TELEMETRY;
@@ -367,6 +368,9 @@ void Engine::alloc_device() {
     E_.window_ns = opts_.window_ns;
   }
   E_.exit_flag = static_cast<uint32_t*>(dev(sizeof(uint32_t)));
+  E_.board_hbm = static_cast<int64_t*>(dev(sizeof(int64_t) * kMaxRails));
+  E_.board = nullptr;
+  E_.omega = 0.0;  // until a board is attached (scheduler.cpp:110: no board, local queue only)
   E_.has_ce = has_ce_ ? 1u : 0u;
   E_.work_cap = opts_.work_capacity;
   E_.work = static_cast<WorkItem*>(dev(sizeof(WorkItem) * opts_.work_capacity));
@@ -518,6 +522,7 @@ void Engine::free_device() {
   xc_ring_ = nullptr;
   for (auto& kv : segs_)
     for (void* p : kv.second.registered) cudaHostUnregister(p);
+  if (board_registered_) cudaHostUnregister(board_registered_), board_registered_ = nullptr;
   for (auto& s : ce_streams_)
     if (s) cudaStreamDestroy(s);
   ce_streams_.clear();
@@ -807,6 +812,45 @@ std::string Engine::telemetry_csv() {
     }
   }
   return out;
+}
+
+// ------------------------------------------------------------------ global load board
+
+size_t board_bytes(uint32_t n_slots) { return sizeof(BoardSlot) * n_slots; }
+
+void Engine::attach_board(void* board, uint32_t n_slots, uint32_t slot, uint64_t period_ns) {
+  std::lock_guard<std::mutex> lk(mu_);
+  if (!started_) throw EngineError("engine not started");
+  if (!board) throw ConfigError("load board: null board");
+  if (n_slots == 0 || slot >= n_slots) throw ConfigError("load board: slot out of range");
+  if (period_ns == 0) throw ConfigError("load board: publish period must be > 0");
+  if (E_.board) throw EngineError("load board: already attached");
+  for (const auto& kv : batches_) {
+    volatile BatchDev* m = &bmirror_[kv.second.slot];
+    if (m->failed_id != kv.second.id && m->done - kv.second.base < kv.second.submitted)
+      throw EngineError("load board: attach while no batch is in flight");
+  }
+  CK(cudaSetDevice(device_));
+  void* dp = nullptr;
+  if (cudaHostGetDevicePointer(&dp, board, 0) != cudaSuccess) {  // not pinned yet: map it
+    cudaGetLastError();
+    CK(cudaHostRegister(board, board_bytes(n_slots), cudaHostRegisterMapped | cudaHostRegisterPortable));
+    board_registered_ = board;
+    CK(cudaHostGetDevicePointer(&dp, board, 0));
+  }
+  // the running kernel holds the previous EngineDev: let it exit, the next launch has the board
+  if (ctl_->state != 0) {
+    ctl_->stop = 1;
+    std::atomic_thread_fence(std::memory_order_seq_cst);
+    CK(cudaStreamSynchronize(stream_));
+    ctl_->stop = 0;
+    ctl_->state = 0;
+  }
+  E_.board = static_cast<BoardSlot*>(dp);
+  E_.board_slots = n_slots;
+  E_.board_slot = slot;
+  E_.board_period = period_ns;
+  E_.omega = opts_.diffusion_weight;
 }
 
 // ------------------------------------------------------------------ dataflow gates

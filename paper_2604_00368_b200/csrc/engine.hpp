@@ -47,6 +47,7 @@ struct EngineOptions {
 // engine_options_from_json (engine.cpp:1199-1307): unknown keys rejected.
 EngineOptions engine_options_from_json(const std::string& text);
 void default_sched_config(spray_sched_config* c);
+size_t board_bytes(uint32_t n_slots);  // spray_board_bytes
 void default_resilience_config(spray_resilience_config* c);
 
 class Engine {
@@ -108,6 +109,8 @@ class Engine {
   // `flags` = one uint32 counter per chunk_bytes granule, device memory reachable from this
   // GPU (the producer's and the consumer's engines share it).
   void gate_segment(const std::string& seg_id, uint32_t role, void* flags);
+  // GlobalLoadBoard (scheduler.hpp:66-90): publish/blend through a shared host board
+  void attach_board(void* board, uint32_t n_slots, uint32_t slot, uint64_t period_ns);
   // TelemetrySnapshot::to_csv columns from the device's per-rail window cells.
   std::string telemetry_csv();
   // Diagnostic snapshot: host/device ring positions, kernel state, counters, stream status.
@@ -183,6 +186,7 @@ class Engine {
     std::vector<void*> via_allocs;    // staging, descriptors, exit generation
   };
   std::vector<RelayHost> relays_;
+  void* board_registered_ = nullptr;  // host board this engine registered (unregistered on free)
   uint32_t launch_gen_ = 0;
   void setup_relay(uint32_t idx, int via);
   void sync_relays();

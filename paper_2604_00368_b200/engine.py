@@ -297,6 +297,12 @@ class Engine:
     # ---- dataflow gates (forwarding / relays / broadcast chains)
     GATE_CONSUME, GATE_PRODUCE = 1, 2
 
+    def attach_board(self, board_ptr: int, n_slots: int, slot: int, period_ns: int = 10_000_000):
+        """GlobalLoadBoard (scheduler.hpp:66-90): publish this engine's per-rail queued bytes
+        into `slot` of a zeroed host board of board_bytes(n_slots) bytes every period and
+        blend the fresh entries in with scheduler.diffusion_weight."""
+        _check(lib.spray_engine_attach_board(self._h, board_ptr, n_slots, slot, period_ns))
+
     def gate_segment(self, segment_id: str, role: int, flags_ptr: int):
         """Gate a registered single-buffer segment: `flags_ptr` points at one zeroed uint32
         counter per chunk_bytes() granule, shared by the producing and consuming engines."""
@@ -519,6 +525,11 @@ def host_alloc(n: int) -> int:
 
 def host_free(p: int):
     _check(lib.spray_host_free(p))
+
+
+def board_bytes(n_slots: int) -> int:
+    """Size of a load board with n_slots engine instances (spray_board_bytes)."""
+    return int(lib.spray_board_bytes(n_slots))
 
 
 IPC_HANDLE_BYTES = 72  # SPRAY_IPC_HANDLE_BYTES: CUDA IPC handle + offset inside the allocation

@@ -70,6 +70,30 @@ def replay_fixtures(ref, co):
                                    decisions=out["decisions"], queued=out["queued"], beta=out["beta"],
                                    health=out["health"], expect_failures=out["expect_failures"],
                                    bw=bw, tier=tier, rank=rank)
+    # GlobalLoadBoard cases (scheduler.cpp:63-79, 108-114): omega > 0 with BOARD events;
+    # a separate generator so the cases above stay as they were
+    rng = np.random.default_rng(2027)
+    for case in range(24, 32):
+        topo = spraygen.random_doc(rng)
+        policy = [0, 0, 1, 2][case % 4]
+        omega = [0.25, 0.5, 0.9, 1.0][case % 4]
+        sc = sched_config(policy=policy, tolerance=[0.05, 1e-9][case % 2], omega=omega)
+        rc = res_config()
+        bw, tier, rank, ids = ref.rails(topo)
+        sim_caps = caps("sim", **spraygen.SIM_CAPS)
+        try:
+            s_w = cands_for(ref, topo, [sim_caps], 1, sc=sc)
+            s_r = cands_for(ref, topo, [sim_caps], 0, sc=sc)
+        except RuntimeError:
+            continue
+        stream = spraygen.stream_concat([s_w, s_r])
+        st = CState(co, sc, rc, bw, tier, rank, stream)
+        events = spraygen.random_trace(rng, st, 2, len(bw), bw, 1500, board=True)
+        out = ref.replay(topo, sc, rc, stream, events, len(bw))
+        cases[f"case{case}"] = dict(topo=topo, sc=bytes(sc), rc=bytes(rc), stream=stream, events=events,
+                                   decisions=out["decisions"], queued=out["queued"], beta=out["beta"],
+                                   health=out["health"], expect_failures=out["expect_failures"],
+                                   bw=bw, tier=tier, rank=rank)
     np.savez_compressed(os.path.join(OUT, "replay.npz"),
                         **{f"{k}__{f}": (np.frombuffer(v, np.uint8) if isinstance(v, bytes)
                                          else np.array(v)) for k, d in cases.items() for f, v in d.items()})

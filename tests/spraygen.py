@@ -10,7 +10,7 @@ import json
 
 import numpy as np
 
-from oracle.oracle import (EV_CHARGE, EV_COMPLETE, EV_DECIDE, EV_DUE_PROBES, EV_EXPECT, EV_HEALTH,
+from oracle.oracle import (EV_BOARD, EV_CHARGE, EV_COMPLETE, EV_DECIDE, EV_DUE_PROBES, EV_EXPECT, EV_HEALTH,
                            EV_PROBE_DONE, EV_RELEASE, EV_RESET, EV_RESET_RAIL, EVENT_DTYPE, EVF_CANCELLED,
                            EVF_MODEL, NO_RAIL)
 
@@ -48,16 +48,29 @@ def random_doc(rng: np.random.Generator, backend="sim"):
 
 
 def random_trace(rng: np.random.Generator, cstate, n_sets: int, n_rails: int, bw, n_events: int,
-                 health_changes=True, resets=True):
+                 health_changes=True, resets=True, board=False):
     """Realistic event stream: decisions, completions of earlier decisions (OK, FAILED,
-    with/without feedback), retries as CHARGE, health flips, periodic resets. `cstate`
-    (oracle.CState) is stepped alongside so completions release what was charged."""
+    with/without feedback), retries as CHARGE, health flips, periodic resets, and (board)
+    load-board refreshes: one BOARD event per rail carrying a global queue that is this
+    instance's queue plus other instances' load. `cstate` (oracle.CState) is stepped
+    alongside so completions release what was charged."""
     events = []
     outstanding = []   # (local, remote, len, predicted, x, model)
     probes = []        # rails with a probe in flight
     now = 0
     for _ in range(n_events):
         now += int(rng.integers(1_000, 200_000))
+        if board and rng.random() < 0.04:
+            _, queued, _, _, _ = cstate.step(np.zeros(0, EVENT_DTYPE))
+            for r in range(n_rails):
+                other = int(rng.choice([0, 0, int(rng.integers(0, 1 << 24)), int(rng.integers(0, 1 << 30))]))
+                b = np.zeros(1, EVENT_DTYPE)
+                b["kind"] = EV_BOARD
+                b["rail"] = r
+                b["len"] = max(0, int(queued[r])) + other
+                b["now_ns"] = now
+                cstate.step(b)
+                events.append(b[0])
         u = rng.random()
         e = np.zeros(1, EVENT_DTYPE)
         if u < 0.45 or not outstanding:

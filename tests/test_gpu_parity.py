@@ -654,3 +654,42 @@ def test_transport_backend_plugin():
     assert be.fatal() and be.post_slices(reqs[:1]).fatal
     be.stop()
     be.close()
+
+
+# ------------------------------------------------------------------ global load board
+def test_load_board_steers_and_replays_identically(co):
+    """GlobalLoadBoard (scheduler.cpp:63-79, 108-114; engine.cpp:1090-1093): another
+    instance's slot reports rail a.r0 heavily loaded, so with diffusion_weight 0.5 this
+    engine sprays onto a.r1. The engine publishes its own slot; its live trace (BOARD
+    events included) replays identically through the C oracle and the device replay."""
+    topo = fabrics.two_node(2, 1e9, backend="cuda")
+    e = make_engine(topo, {"resilience": {"degradation_ratio": 1e9}, "scheduler": {"diffusion_weight": 0.5},
+                           "b200": {"chunk_bytes": 65536}})
+    nslot = 2
+    board = torch.zeros(sp.board_bytes(nslot), dtype=torch.uint8, pin_memory=True)
+    words = board.view(torch.int64).view(nslot, -1)  # [heartbeat, pad, queued[64]] per slot
+    words[1, 0] = (1 << 62)           # the other instance's heartbeat: never stale
+    words[1, 2 + 0] = 1 << 34         # ... and its queue on rail a.r0 (index 0)
+    e.attach_board(board.data_ptr(), nslot, 0, 1_000_000)
+    e.trace_enable(1 << 18)
+    n = 64 << 20
+    src, dst = dev_buf(n, 41), dev_buf(n)
+    e.register_segment(sp.SegmentDescriptor("s", sp.Medium.DEVICE, "a", [sp.BufferDesc(0, n, src.data_ptr())]))
+    e.register_segment(sp.SegmentDescriptor("d", sp.Medium.DEVICE, "b", [sp.BufferDesc(0, n, dst.data_ptr())]))
+    import time
+    for k in range(4):
+        b = e.allocate_batch()
+        e.submit_transfers(b, [sp.TransferRequest("s", i * (n // 8), "d", i * (n // 8), n // 8) for i in range(8)])
+        assert e.await_batch(b, 30_000_000_000).state == sp.BatchState.COMPLETE
+        e.free_batch(b)
+        time.sleep(0.003)  # the board refreshes every 1 ms
+    assert torch.equal(src, dst)
+    by = {e.rail_id(r): e.rail_stats(r).bytes_ok for r in range(e.rail_count())}
+    assert by["a.r1"] > 0.9 * (by["a.r0"] + by["a.r1"]), by
+    assert int(words[0, 0]) != 0  # this engine published its slot
+    bw, tier, rank = rails_of(topo)
+    ev, _ = replay_live(co, e, sched_config(omega=0.5), res_config(degradation_ratio=1e9), bw, tier, rank)
+    from oracle.oracle import EV_BOARD
+    boards = ev[ev["kind"] == EV_BOARD]
+    assert len(boards) >= 2 and (boards["len"][boards["rail"] == 0] >= (1 << 34)).all()
+    e.stop()

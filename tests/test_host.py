@@ -78,7 +78,7 @@ def test_kv_fabric_routes_host_only_over_pcie_rails():
     ({"resilience": {"failure_threshold": 0}}, "failure threshold"),
     ({"clock": "virtual"}, "clock"),
     ({"b200": {"chunk_bytes": 12345}}, "power of two"),
-    ({"scheduler": {"diffusion_weight": 0.5}}, "diffusion"),
+    ({"scheduler": {"diffusion_weight": 1.5}}, "diffusion"),  # scheduler.cpp:39-40
 ])
 def test_config_errors(cfg, msg):
     with pytest.raises(sp.ConfigError, match=msg):

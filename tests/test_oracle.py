@@ -7,7 +7,7 @@ import os
 import numpy as np
 import pytest
 
-from oracle.oracle import (EVENT_DTYPE, EV_CHARGE, EV_COMPLETE, EV_DECIDE, EV_EXPECT, EV_HEALTH, EV_RELEASE,
+from oracle.oracle import (EVENT_DTYPE, EV_BOARD, EV_CHARGE, EV_COMPLETE, EV_DECIDE, EV_EXPECT, EV_HEALTH, EV_RELEASE,
                            EV_RESET, EVF_MODEL, CState, ResConfig, SchedConfig, ref_available, res_config,
                            sched_config)
 
@@ -317,3 +317,61 @@ def test_c_oracle_vs_reference_fresh_traces(co):
         b = co.replay(sc, rc, bw, tier, rank, stream, events)
         assert a["decisions"].tobytes() == b["decisions"].tobytes()
         assert a["beta"].tobytes() == b["beta"].tobytes()
+
+
+# ------------------------------------------------------------------ global load board
+def test_load_board_blends_into_effective_queue(co):
+    """test_scheduler.cpp:389-403: another instance reports rail 0 loaded (100000 B), so
+    with omega 0.5 the decision steers to rail 1; without the board (omega 0) it does not.
+    The BOARD event carries global_queued(rail) = own published + others."""
+    bw, tier, rank, stream = _two_rail(tier2=False)
+    bw = [1000.0] * 4
+    trace = cat(ev(EV_BOARD, 0, len=100000), ev(EV_BOARD, 1, len=0), ev(EV_DECIDE, 0, len=100))
+    on = co.replay(sched_config(omega=0.5), res_config(), bw, tier, rank, stream, trace)
+    off = co.replay(sched_config(omega=0.0), res_config(), bw, tier, rank, stream, trace)
+    assert on["decisions"][0]["local"] == 1
+    assert off["decisions"][0]["local"] == 0
+    # x = ((1 - w) * local + w * global + L) / B for the picked rail (global 0 there)
+    assert on["decisions"][0]["x_norm"] == (0.5 * 0.0 + 0.5 * 0.0 + 100.0) / 1000.0
+    if ref_available():
+        import spraygen
+        from oracle.oracle import RefOracle
+        ref = RefOracle()
+        topo = spraygen.two_node_doc(2, 1000.0)
+        a = ref.replay(topo, sched_config(omega=0.5), res_config(), stream, trace, 4)
+        assert a["decisions"].tobytes() == on["decisions"].tobytes()
+
+
+def test_load_board_golden_cases_depend_on_the_board(co, golden_dir):
+    """The omega > 0 goldens are not vacuous: for a board refresh, replaying the prefix
+    that ends with the decisions after it, with that one refresh's global queues zeroed,
+    decides differently. (Before that refresh both replays see the same board, so each
+    prefix stays a consistent trace.)"""
+    z, cases = _cases(golden_dir)
+    n_board = n_diff = 0
+    for c in cases:
+        sc = SchedConfig.from_buffer_copy(z[c + "__sc"].tobytes())
+        if not sc.diffusion_weight > 0:
+            continue
+        n_board += 1
+        ev_ = z[c + "__events"]
+        rc = ResConfig.from_buffer_copy(z[c + "__rc"].tobytes())
+        args = (z[c + "__bw"], z[c + "__tier"], z[c + "__rank"], z[c + "__stream"])
+        kinds = ev_["kind"]
+        starts = [i for i in np.nonzero(kinds == EV_BOARD)[0] if i == 0 or kinds[i - 1] != EV_BOARD]
+        for b in starts:
+            k = int(b)
+            while k < len(ev_) and kinds[k] == EV_BOARD:
+                k += 1
+            end = k
+            while end < len(ev_) and kinds[end] in (EV_DECIDE, EV_CHARGE, EV_RELEASE):
+                end += 1
+            pre = ev_[:end].copy()
+            on = co.replay(sc, rc, *args, pre)
+            assert on["decisions"].tobytes() == z[c + "__decisions"][:len(on["decisions"])].tobytes()
+            pre["len"][b:k] = 0
+            off = co.replay(sc, rc, *args, pre)
+            if off["decisions"].tobytes() != on["decisions"].tobytes():
+                n_diff += 1
+                break
+    assert n_board >= 6 and n_diff >= n_board - 1
