@@ -47,6 +47,8 @@ def engine(dev, gpus, sm_rails, ce_rails, extra_cfg=None):
     cfg = {"resilience": {"degradation_ratio": 1e9}}
     if RELAY.get("chunk"):
         cfg["b200"] = {"chunk_bytes": RELAY["chunk"]}
+    if RELAY.get("max_slices"):
+        cfg["scheduler"] = {"max_slices_per_transfer": RELAY["max_slices"]}
     cfg.update(extra_cfg or {})
     e = sp.Engine(fabrics.peer_fabric(gpus, sm_rails=sm_rails, ce_rails=ce_rails, bw_ce=CE_GBS * 1e9,
                                       relay_via=RELAY["via"], relay_affinity=RELAY["affinity"]),
@@ -368,10 +370,12 @@ def main():
     ap.add_argument("--relay-affinity", default="same_socket", help="relay rail tier (direct = tier 1)")
     ap.add_argument("--chunk-kib", type=int, default=0, help="b200.chunk_bytes (SM work granule), KiB")
     ap.add_argument("--congest-rail", default="g0.nvl0", help="congest: the DEGRADEd rail")
+    ap.add_argument("--max-slices", type=int, default=0, help="scheduler.max_slices_per_transfer (diagnostic)")
     ap.add_argument("--factor", type=float, default=0.25, help="congest: bandwidth factor of the DEGRADEd rail")
     args = ap.parse_args()
     RELAY["via"], RELAY["affinity"] = args.relay_via, args.relay_affinity
     RELAY["chunk"] = args.chunk_kib << 10 if args.chunk_kib else 0
+    RELAY["max_slices"] = args.max_slices
     global CE_GBS
     CE_GBS = args.ce_gbs
     out = {"c2": c2, "elephant": elephant, "c4": c4, "c4chain": c4chain, "c5": c5, "congest": congest}[args.mode](args)
