@@ -51,6 +51,8 @@ def parse():
     p.add_argument("--no-nvlink", action="store_true", help="N>1: skip the NVLink phase (elephant, broadcast chain, fault)")
     p.add_argument("--nvl-bytes", type=int, default=1 << 30, help="N>1: bytes per elephant flow (C2 shape)")
     p.add_argument("--bcast-bytes", type=int, default=16 << 30, help="N>1: broadcast size (C4 shape)")
+    p.add_argument("--nvl-mode", default="push", choices=["pull", "push"],
+                   help="N>1: which end's engine moves elephant flows and chain hops")
     return p.parse_args()
 
 
@@ -295,19 +297,33 @@ def nvlink_phase(sp, fabrics, args, rank, world, dev):
     def seg(e, sid, g, n, ptr):
         e.register_segment(sp.SegmentDescriptor(sid, sp.Medium.DEVICE, f"g{g}", [sp.BufferDesc(0, n, ptr)]))
 
-    # ---- elephant flows
+    # ---- elephant flows. push (default): the sender's engine moves each flow (peer
+    # stores); pull: the receiver's (peer loads, storing locally). A lone flow pulls faster
+    # (peer loads reach the copy-engine ceiling, ~786 GB/s, where peer stores stop at ~709:
+    # tools/peer_pull.cu), but in the ring, where every GPU sends and receives at once,
+    # push measured 636 GB/s per flow against 572 for pull (4 x B200).
+    pull = args.nvl_mode == "pull"
     n = args.nvl_bytes
     src = torch.empty(n, dtype=torch.uint8, device=f"cuda:{dev}")
     sp.fill_splitmix(dev, src.data_ptr(), n, 500 + rank)
     dst = torch.zeros(n, dtype=torch.uint8, device=f"cuda:{dev}")
-    hs = gather(sp.ipc_export(dev, dst.data_ptr()))
-    pdst = open_peer(hs[nxt])
+    hs = gather((sp.ipc_export(dev, src.data_ptr()), sp.ipc_export(dev, dst.data_ptr())))
+    pdst = open_peer(hs[nxt][1])
     cfg = json.dumps({"resilience": {"degradation_ratio": 1e9}})
-    e = sp.Engine(fabrics.peer_fabric(sorted({rank, nxt})), cfg, dev)
-    e.start()
-    seg(e, f"src{rank}", rank, n, src.data_ptr())
-    seg(e, f"dst{nxt}", nxt, n, pdst)
-    prep = e.prepare_transfers([sp.TransferRequest(f"src{rank}", 0, f"dst{nxt}", 0, n)])
+    ecfg = json.dumps({"resilience": {"degradation_ratio": 1e9}, "b200": {"chunk_bytes": 65536 if pull else 32768}})
+    if pull:
+        e = sp.Engine(fabrics.peer_fabric(sorted({prv, rank})), ecfg, dev)
+        e.start()
+        seg(e, f"src{prv}", prv, n, open_peer(hs[prv][0]))
+        seg(e, f"dst{rank}", rank, n, dst.data_ptr())
+        flow = sp.TransferRequest(f"src{prv}", 0, f"dst{rank}", 0, n)
+    else:
+        e = sp.Engine(fabrics.peer_fabric(sorted({rank, nxt})), ecfg, dev)
+        e.start()
+        seg(e, f"src{rank}", rank, n, src.data_ptr())
+        seg(e, f"dst{nxt}", nxt, n, pdst)
+        flow = sp.TransferRequest(f"src{rank}", 0, f"dst{nxt}", 0, n)
+    prep = e.prepare_transfers([flow])
     times = []
     for k in range(args.warmup + max(3, args.steps)):
         torch.cuda.synchronize(dev)
@@ -325,12 +341,16 @@ def nvlink_phase(sp, fabrics, args, rank, world, dev):
     exact = allok(sp.checksum(dev, dst.data_ptr(), n) == sums[prv])
     mean = statistics.mean(times)
     out["elephant"] = {"flows": f"{world} x (r -> r+1 mod {world})", "bytes_per_flow": n, "slices_per_flow": 4096,
-                       "rails": "1 SM peer-store rail per GPU", "ms_max_over_ranks": round(mean, 4),
+                       "rails": ("1 SM rail per GPU, driven by the receiver (peer loads), 64 KiB granules" if pull
+                                 else "1 SM rail per GPU, driven by the sender (peer stores), 32 KiB granules"),
+                       "ms_max_over_ranks": round(mean, 4),
                        "aggregate_gbs": GBs(world * n, mean), "per_flow_gbs": GBs(n, mean),
                        "best_aggregate_gbs": GBs(world * n, min(times)),
                        "roofline": {"peak_gbs": 900.0 * world, "unit": "GB/s",
                                     "frac": round(world * n / (mean * 1e-3) / 1e9 / (900.0 * world), 4),
-                                    "peak_source": "nominal NVLink 5, 900 GB/s per direction per GPU"},
+                                    "peak_source": "nominal NVLink 5, 900 GB/s per direction per GPU",
+                                    "measured_ceiling_gbs_per_flow": {"sm_peer_loads": 786, "copy_engine": 782,
+                                                                      "sm_peer_stores": 709}},
                        "bit_exact": exact}
     prep.free()
     e.stop()
@@ -347,7 +367,22 @@ def nvlink_phase(sp, fabrics, args, rank, world, dev):
     flags = torch.zeros(nb_ // cb, dtype=torch.int32, device=f"cuda:{dev}")
     hs = gather((sp.ipc_export(dev, w.data_ptr()), sp.ipc_export(dev, flags.data_ptr())))
     ec, pc = None, None
-    if rank + 1 < world:
+    if pull and rank > 0:
+        # rank k pulls w_{k-1} -> w_k: it waits granule by granule for rank k-1 to have
+        # delivered w_{k-1} (CONSUME, counters in this GPU's HBM, written by rank k-1) and
+        # signals rank k+1 (PRODUCE into rank k+1's counters)
+        pw = open_peer(hs[rank - 1][0])
+        ec = sp.Engine(fabrics.peer_fabric(sorted({rank - 1, rank})), chain_cfg, dev)
+        ec.start()
+        seg(ec, f"w{rank - 1}", rank - 1, nb_, pw)
+        seg(ec, f"w{rank}", rank, nb_, w.data_ptr())
+        if rank > 1:
+            ec.gate_segment(f"w{rank - 1}", sp.Engine.GATE_CONSUME, flags.data_ptr())
+        if rank + 1 < world:
+            ec.gate_segment(f"w{rank}", sp.Engine.GATE_PRODUCE, open_peer(hs[rank + 1][1]))
+        pc = ec.prepare_transfers([sp.TransferRequest(f"w{rank - 1}", 0, f"w{rank}", 0, nb_)])
+    elif not pull and rank + 1 < world:
+        # rank k pushes w_k -> w_{k+1} and signals rank k+1 (PRODUCE into its counters)
         pw, pf = open_peer(hs[rank + 1][0]), open_peer(hs[rank + 1][1])
         ec = sp.Engine(fabrics.peer_fabric(sorted({rank, rank + 1})), chain_cfg, dev)
         ec.start()
@@ -408,6 +443,8 @@ def nvlink_phase(sp, fabrics, args, rank, world, dev):
     fexact = allok(sp.checksum(dev, w.data_ptr(), nb_) == ref)
     cm = statistics.mean(ctimes)
     out["bcast"] = {"bytes": nb_, "receivers": world - 1, "dtype": "bf16 bit patterns moved as bytes",
+                    "chain": ("each hop pulled by the receiving GPU's engine" if pull else
+                              "each hop pushed by the forwarding GPU's engine") + ", 64 KiB gated granules",
                     "chain_ms": round(cm, 3), "chain_delivered_gbs": GBs((world - 1) * nb_, cm),
                     "chain_per_receiver_gbs": GBs(nb_, cm), "chain_bit_exact": exact,
                     "fanout_ms": round(ftime, 3) if ftime else None,

@@ -78,8 +78,11 @@ def timed_prepared(e, reqs, reps):
 def c2(args):
     n = args.size
     src, dst = buf(0, n, 77), buf(1, n)
-    out = {"mode": "c2", "bytes": n, "slices": 4096, "sm_rails": args.sm_rails, "ce_rails": args.ce_rails}
-    e = engine(0, [0, 1], args.sm_rails, args.ce_rails)
+    out = {"mode": "c2", "bytes": n, "slices": 4096, "sm_rails": args.sm_rails, "ce_rails": args.ce_rails,
+           "pull": bool(args.pull)}
+    # --pull: the engine (and so the copying SMs) sits on the destination GPU, which loads
+    # from peer HBM and stores locally
+    e = engine(1 if args.pull else 0, [0, 1], args.sm_rails, args.ce_rails)
     reg(e, "src", 0, src)
     reg(e, "dst", 1, dst)
     req = [sp.TransferRequest("src", 0, "dst", 0, n)]
@@ -371,6 +374,7 @@ def main():
     ap.add_argument("--chunk-kib", type=int, default=0, help="b200.chunk_bytes (SM work granule), KiB")
     ap.add_argument("--congest-rail", default="g0.nvl0", help="congest: the DEGRADEd rail")
     ap.add_argument("--max-slices", type=int, default=0, help="scheduler.max_slices_per_transfer (diagnostic)")
+    ap.add_argument("--pull", action="store_true", help="c2: run the engine on the destination GPU (peer loads)")
     ap.add_argument("--factor", type=float, default=0.25, help="congest: bandwidth factor of the DEGRADEd rail")
     args = ap.parse_args()
     RELAY["via"], RELAY["affinity"] = args.relay_via, args.relay_affinity
