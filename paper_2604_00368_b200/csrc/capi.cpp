@@ -241,17 +241,7 @@ int spray_run_prepared(spray_engine* e, uint64_t batch, spray_prepared* p, float
     // make sure no launch is resident, so this one is bracketed alone
     while (g.running_kernel()) std::this_thread::sleep_for(std::chrono::microseconds(50));
     CK(cudaStreamSynchronize(g.stream()));
-    cudaEvent_t a, b;
-    CK(cudaEventCreate(&a));
-    CK(cudaEventCreate(&b));
-    CK(cudaEventRecord(a, g.stream()));
-    g.submit_device_intents(batch, p->dev, p->n, p->slices);  // publishes + launches (drain mode)
-    CK(cudaEventRecord(b, g.stream()));
-    CK(cudaEventSynchronize(b));
-    float ms = 0.f;
-    CK(cudaEventElapsedTime(&ms, a, b));
-    cudaEventDestroy(a);
-    cudaEventDestroy(b);
+    const float ms = g.run_device_intents_timed(batch, p->dev, p->n, p->slices);  // one drain-mode launch
     g.set_drain(false);
     if (kernel_ms) *kernel_ms = ms;
   });

@@ -188,6 +188,10 @@ struct alignas(64) Control {
   // scheduler profile (globaltimer ns): loops, time in completions / submissions / control
   volatile uint64_t prof_loops, prof_comp_ns, prof_sub_ns, prof_ctl_ns, prof_n_comp, prof_n_dec;
   volatile uint64_t prof_x[16];      // fine-grained scheduler phase clocks (SM cycles) and counts
+  // per-launch timeline (engine ns): 0 scheduler start, 1 first work items stamped,
+  // 2 first decision, 3 last decision, 4 first completion applied, 5 last completion
+  // applied, 6 scheduler exit
+  volatile uint64_t tl[8];
 };
 
 // Telemetry window cell (telemetry.hpp:37-44 WindowCell), one per rail per window in an
@@ -251,6 +255,16 @@ struct BoardSlot {
   int64_t queued[kMaxRails];
 };
 
+// The device-written control-block words a launch resumes from, snapshotted by the host
+// at launch (no kernel is resident then): reading them from mapped host memory at kernel
+// start cost one PCIe round trip each on the scheduler's critical path.
+struct LaunchSnap {
+  uint64_t sub_head, bulk_done, xc_head, ce_tail[8], idle_exit_ns;
+  uint64_t bytes_dispatched, bytes_terminated, batches_failed;
+  uint64_t heal_fault_start, heal_first_ok, failed_attempts, retried_ok, trace_n, trace_dn;
+  uint32_t drain, trace_on;
+};
+
 // Everything the kernel needs, passed by value.
 struct EngineDev {
   Control* ctl;                      // mapped host
@@ -308,6 +322,7 @@ struct EngineDev {
   int64_t* board_hbm;                          // HBM: the adopted global view, kept across launches
   uint32_t board_slots, board_slot;
   uint64_t board_period;                       // publish period, ns (staleness = 3 periods)
+  LaunchSnap snap;                             // control-block words at launch (host snapshot)
 };
 
 // scalars persisted in EngineDev::persist between launches

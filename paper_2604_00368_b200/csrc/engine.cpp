@@ -14,6 +14,7 @@ size_t engine_smem_bytes();
 cudaError_t launch_engine(const spray_dev::EngineDev& E, int grid, int block, cudaStream_t st);
 cudaError_t launch_epoch(uint64_t* out, cudaStream_t st);
 cudaError_t launch_relay_forward(const spray_dev::EngineDev& E, uint32_t r, int grid, cudaStream_t st);
+cudaError_t launch_hold(const uint32_t* flag, cudaStream_t st);
 }  // namespace spray_launch
 
 namespace spray {
@@ -523,6 +524,7 @@ void Engine::free_device() {
   for (auto& kv : segs_)
     for (void* p : kv.second.registered) cudaHostUnregister(p);
   if (board_registered_) cudaHostUnregister(board_registered_), board_registered_ = nullptr;
+  if (hold_) cudaFreeHost(const_cast<uint32_t*>(hold_)), hold_ = nullptr, hold_dev_ = nullptr;
   for (auto& s : ce_streams_)
     if (s) cudaStreamDestroy(s);
   ce_streams_.clear();
@@ -590,6 +592,25 @@ void Engine::launch() {
   std::atomic_thread_fence(std::memory_order_seq_cst);
   sync_relays();
   E_.launch_gen = ++launch_gen_;
+  {  // the device-written words this launch resumes from (no kernel is resident now)
+    LaunchSnap& sn = E_.snap;
+    sn.sub_head = ctl_->sub_head;
+    sn.bulk_done = ctl_->bulk_done;
+    sn.xc_head = ctl_->xc_head;
+    for (int k = 0; k < 8; ++k) sn.ce_tail[k] = ctl_->ce_tail[k];
+    sn.idle_exit_ns = ctl_->idle_exit_ns;
+    sn.bytes_dispatched = ctl_->bytes_dispatched;
+    sn.bytes_terminated = ctl_->bytes_terminated;
+    sn.batches_failed = ctl_->batches_failed;
+    sn.heal_fault_start = ctl_->heal_fault_start;
+    sn.heal_first_ok = ctl_->heal_first_ok;
+    sn.failed_attempts = ctl_->failed_attempts;
+    sn.retried_ok = ctl_->retried_ok;
+    sn.trace_n = ctl_->trace_n;
+    sn.trace_dn = ctl_->trace_dn;
+    sn.drain = ctl_->drain;
+    sn.trace_on = ctl_->trace_on;
+  }
   CK(spray_launch::launch_engine(E_, grid, opts_.block, stream_));
   for (uint32_t r = 0; r < relays_.size(); ++r) {  // hop 2 on each relay GPU
     CK(cudaSetDevice(relays_[r].via));
@@ -1115,6 +1136,53 @@ void Engine::submit_device_intents(uint64_t batch, const void* dev_intents, uint
   publish(&bulk, 1);
 }
 
+// Prepared (device-resident) intents, timed: the caller guarantees no launch is resident
+// and the stream is idle. The bulk descriptor is published first; then the stream is held
+// on a mapped flag while the bracket (event, launch, event) is enqueued, and released, so
+// the events time the engine kernel and not the host's launch latency.
+float Engine::run_device_intents_timed(uint64_t batch, const void* dev_intents, uint64_t n, uint64_t total_slices) {
+  std::lock_guard<std::mutex> lk(mu_);
+  if (ctl_->state != 0) throw EngineError("timed run: a launch is still resident");
+  BatchRec& b = batch_ref(batch);
+  b.submitted += total_slices;
+  Intent bulk{};
+  bulk.batch_id = b.id;
+  bulk.src = reinterpret_cast<uint64_t>(dev_intents);
+  bulk.len = n;
+  bulk.batch_slot = b.slot;
+  bulk.flags = kIntentBulk;
+  ring_[sub_tail_ % opts_.sub_capacity] = bulk;
+  ++sub_tail_;
+  std::atomic_thread_fence(std::memory_order_release);
+  ctl_->sub_tail = sub_tail_;
+  CK(cudaSetDevice(device_));
+  if (!hold_) {
+    void* h = nullptr;
+    void* d = nullptr;
+    CK(cudaHostAlloc(&h, sizeof(uint32_t), cudaHostAllocMapped | cudaHostAllocPortable));
+    CK(cudaHostGetDevicePointer(&d, h, 0));
+    hold_ = static_cast<volatile uint32_t*>(h);
+    hold_dev_ = static_cast<uint32_t*>(d);
+  }
+  *hold_ = 0;
+  std::atomic_thread_fence(std::memory_order_seq_cst);
+  cudaEvent_t a, z;
+  CK(cudaEventCreate(&a));
+  CK(cudaEventCreate(&z));
+  CK(spray_launch::launch_hold(hold_dev_, stream_));
+  CK(cudaEventRecord(a, stream_));
+  launch();
+  CK(cudaEventRecord(z, stream_));
+  std::atomic_thread_fence(std::memory_order_seq_cst);
+  *hold_ = 1;
+  CK(cudaEventSynchronize(z));
+  float ms = 0.f;
+  CK(cudaEventElapsedTime(&ms, a, z));
+  cudaEventDestroy(a);
+  cudaEventDestroy(z);
+  return ms;
+}
+
 // ------------------------------------------------------------------ introspection
 
 void Engine::rail_stats(uint32_t rail, spray_rail_stats* out) {
@@ -1185,6 +1253,7 @@ void Engine::debug_words(uint64_t* out, size_t n) {
     v.push_back(static_cast<uint64_t>(ctl_->ce_head[0]));
     v.push_back(static_cast<uint64_t>(ctl_->xc_tail));
     v.push_back(static_cast<uint64_t>(ctl_->xc_head));
+    for (int q = 0; q < 8; ++q) v.push_back(static_cast<uint64_t>(ctl_->tl[q]));  // words 37..44
   }
   for (size_t i = 0; i < n; ++i) out[i] = i < v.size() ? v[i] : 0;
 }

@@ -111,6 +111,8 @@ class Engine {
   void gate_segment(const std::string& seg_id, uint32_t role, void* flags);
   // GlobalLoadBoard (scheduler.hpp:66-90): publish/blend through a shared host board
   void attach_board(void* board, uint32_t n_slots, uint32_t slot, uint64_t period_ns);
+  // prepared intents in one drain-mode launch, timed by CUDA events around the kernel only
+  float run_device_intents_timed(uint64_t batch, const void* dev_intents, uint64_t n, uint64_t total_slices);
   // TelemetrySnapshot::to_csv columns from the device's per-rail window cells.
   std::string telemetry_csv();
   // Diagnostic snapshot: host/device ring positions, kernel state, counters, stream status.
@@ -187,6 +189,8 @@ class Engine {
   };
   std::vector<RelayHost> relays_;
   void* board_registered_ = nullptr;  // host board this engine registered (unregistered on free)
+  volatile uint32_t* hold_ = nullptr;  // mapped flag of the timed-run stream hold
+  uint32_t* hold_dev_ = nullptr;
   uint32_t launch_gen_ = 0;
   void setup_relay(uint32_t idx, int via);
   void sync_relays();

@@ -103,6 +103,9 @@ def c2(args):
                                                                "decide", "ctl", "ingress", "complete", "egress",
                                                                "pub_busy")}
         out["prof_counts"] = {k: d[k] for k in ("loops", "entries", "n_comp", "n_dec", "n_fences")}
+        tl = list(w)[37:44]  # launch timeline (engine ns), relative to the scheduler's start
+        out["timeline_us"] = dict(zip(["first_stamp", "first_decide", "last_decide", "first_apply", "last_apply",
+                                       "exit"], [round((x - tl[0]) / 1e3, 1) if x else None for x in tl[1:]]))
     assert sp.checksum(1, dst.data_ptr(), n) == sp.checksum(0, src.data_ptr(), n)
     # e2e through the public API
     t0 = time.perf_counter()
