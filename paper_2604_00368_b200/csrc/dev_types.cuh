@@ -118,6 +118,9 @@ struct WorkItem {
   uint32_t pad2_;
 };
 static_assert(sizeof(WorkItem) == 48, "work item is 48 B");
+static_assert(offsetof(WorkItem, len) == 16 && offsetof(WorkItem, rail) == 28 && offsetof(WorkItem, remote) == 30 &&
+                  offsetof(WorkItem, attempt) == 32 && offsetof(WorkItem, stamp) == 40,
+              "EGRESS writes work items as two 16-byte vectors + the attempt word");
 
 // Device completion word: one 8-byte store carries slice, status and the publication
 // stamp, so a reader validates and reads it in a single access (no acquire fence).
