@@ -59,6 +59,25 @@ def main():
         out[f"{nint}x{blk >> 10}KiB"] = {"p50_us": round(statistics.median(lat), 1),
                                          "p90_us": round(lat[int(0.9 * len(lat)) - 1], 1),
                                          "submit_us": round(statistics.median(sub), 1)}
+    # one prepared (drain-mode) launch per shape: the scheduler's timeline of that batch
+    import ctypes as C
+    from paper_2604_00368_b200 import _lib as L
+    tls = {}
+    for nint, blk in ((1, 65536), (64, 65536), (1, 4 << 20)):
+        p = e.prepare_transfers([sp.TransferRequest("s", i * blk, "d", i * blk, blk) for i in range(nint)])
+        ms = []
+        for _ in range(5):
+            b = e.allocate_batch()
+            ms.append(p.run(b))
+            e.free_batch(b)
+        w = (C.c_uint64 * 48)()
+        L.lib.spray_engine_debug(e._h, w, 48)
+        tl = list(w)[37:44]
+        tls[f"{nint}x{blk >> 10}KiB"] = {"kernel_us": round(min(ms) * 1e3, 1), **dict(zip(
+            ["first_stamp", "first_decide", "last_decide", "first_apply", "last_apply", "exit"],
+            [round((x - tl[0]) / 1e3, 1) if x else None for x in tl[1:]]))}
+        p.free()
+    out["prepared_timeline_us"] = tls
     e.stop()
     print(json.dumps(out), flush=True)
 
