@@ -42,6 +42,7 @@ def parse():
     p.add_argument("--blocks", type=int, default=4096)
     p.add_argument("--block-kib", type=int, default=64)
     p.add_argument("--group", type=int, default=32, help="offload/reload intents alternate in runs of this size")
+    p.add_argument("--sm-rails", type=int, default=1, help="SM copy rails on the GPU's PCIe root (KV batch)")
     p.add_argument("--ce-rails", type=int, default=0, help="copy-engine rails sprayed beside the SM rail")
     p.add_argument("--ce-gbs", type=float, default=15.0, help="declared bandwidth of each copy-engine rail")
     p.add_argument("--no-cpu-baseline", action="store_true")
@@ -525,7 +526,7 @@ def run_b200(args):
     pool_bytes = blk * nb
 
     cfg = {"resilience": {"degradation_ratio": 1e9}, "b200": {"chunk_bytes": 65536}}
-    eng = sp.Engine(fabrics.kv_offload(dev, sm_rails=1, ce_rails=args.ce_rails, bw_ce=args.ce_gbs * 1e9),
+    eng = sp.Engine(fabrics.kv_offload(dev, sm_rails=args.sm_rails, ce_rails=args.ce_rails, bw_ce=args.ce_gbs * 1e9),
                     json.dumps(cfg), dev)
     eng.start()
     node = f"g{dev}"
@@ -673,7 +674,7 @@ def run_b200(args):
                                    f"{args.block_kib} KiB reload pinned host->HBM per GPU, random block tables, "
                                    f"one batch of {2 * nb} intents per step, offloads and reloads alternating in "
                                    f"runs of {args.group}",
-                       "fabric": f"1 SM PCIe rail + {args.ce_rails} copy-engine rails per GPU (kv_offload)", "bytes_per_step_per_gpu": step_bytes,
+                       "fabric": f"{args.sm_rails} SM PCIe rail(s) + {args.ce_rails} copy-engine rail(s) per GPU (kv_offload)", "bytes_per_step_per_gpu": step_bytes,
                        "l2": "inputs (2 x 256 MiB pools) larger than the 126 MB L2",
                        "parallelism": f"weak x{world} (one batch per GPU, no data-path collective)"},
             "e2e": {"value": round(e2e, 3), "unit": "GB/s",
