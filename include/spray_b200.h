@@ -189,6 +189,17 @@ int spray_heal_stats(spray_engine* e, uint64_t* fault_start_ns, uint64_t* first_
  *                be multiples of chunk_bytes. SM rails only. Register while idle. */
 enum { SPRAY_GATE_CONSUME = 1, SPRAY_GATE_PRODUCE = 2 };
 int spray_gate_segment(spray_engine* e, const char* segment_id, int role, void* flags);
+/* Ring gate: the staged route's bounded staging pool (reference engine.hpp:56-58, 4 MiB
+ * chunks x depth 4 per 64 MiB pool; staged_* in engine.cpp:465-610). The segment's single
+ * buffer (offset 0, a multiple of chunk_bytes) is a ring; intents address a logical window
+ * of `logical_bytes` that wraps onto it (lap = offset / ring bytes), so a transfer of any
+ * size streams through a fixed pool, one transfer per intent at most the ring's size.
+ * `flags` as above; `credits` is one uint32 per granule (zeroed, reachable by both engines):
+ *   CONSUME: a read of lap k waits for flags >= k + 1; completing OK adds 1 to credits.
+ *   PRODUCE: a write of lap k waits for credits >= k (the consumer drained lap k - 1).
+ * Direct SM rails only. Register while idle. logical_bytes == 0 -> SPRAY_ECONFIG. */
+int spray_gate_ring(spray_engine* e, const char* segment_id, int role, void* flags, void* credits,
+                    uint64_t logical_bytes);
 int spray_engine_chunk_bytes(spray_engine* e, uint64_t* out);
 
 /* TelemetrySnapshot::to_csv (telemetry.cpp:123-158): one row per (window, rail),

@@ -8,7 +8,7 @@ from .engine import (BatchState, BatchStatus, BufferDesc, CapabilityError, Compl
                      ConfigError, CudaBackend, CudaError, Direction, Engine, EngineError, FaultEffect, Health,
                      InvalidRangeError, Medium, NoRouteError, PostResult, Prepared, RailStats, Requests,
                      SegmentDescriptor,
-                     SliceWorkRequest, TransferRequest, checksum, fill_splitmix, hash128, host_alloc, host_free, rr_copy,
+                     SliceWorkRequest, StagedRoute, TransferRequest, checksum, fill_splitmix, hash128, host_alloc, host_free, rr_copy,
                      IPC_HANDLE_BYTES, board_bytes, ipc_close, ipc_export, ipc_open)
 from . import fabrics  # noqa: F401
 

@@ -107,6 +107,7 @@ _SIGS = {
     "spray_engine_now_ns": (C.c_uint64, [P]),
     "spray_heal_stats": (C.c_int, [P, U64P, U64P, U64P, U64P]),
     "spray_gate_segment": (C.c_int, [P, C.c_char_p, C.c_int, P]),
+    "spray_gate_ring": (C.c_int, [P, C.c_char_p, C.c_int, P, P, C.c_uint64]),
     "spray_engine_chunk_bytes": (C.c_int, [P, U64P]),
     "spray_board_bytes": (C.c_size_t, [C.c_uint32]),
     "spray_engine_attach_board": (C.c_int, [P, P, C.c_uint32, C.c_uint32, C.c_uint64]),

@@ -155,6 +155,14 @@ int spray_gate_segment(spray_engine* e, const char* segment_id, int role, void* 
   return guard([&] { e->eng->gate_segment(segment_id ? segment_id : "", static_cast<uint32_t>(role), flags); });
 }
 
+int spray_gate_ring(spray_engine* e, const char* segment_id, int role, void* flags, void* credits,
+                    uint64_t logical_bytes) {
+  if (!logical_bytes) return SPRAY_ECONFIG;
+  return guard([&] {
+    e->eng->gate_segment(segment_id ? segment_id : "", static_cast<uint32_t>(role), flags, credits, logical_bytes);
+  });
+}
+
 int spray_telemetry_csv(spray_engine* e, char* buf, size_t cap, size_t* len) {
   return guard([&] {
     const std::string s = e->eng->telemetry_csv();

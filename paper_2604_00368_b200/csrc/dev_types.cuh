@@ -216,15 +216,24 @@ struct TeleCell {
 //            after a system fence (PUBLISH warp).
 enum : uint32_t { kGateConsume = 1, kGateProduce = 2 };
 constexpr int kMaxGates = 4;
+//   Ring gates (ring != 0; the staged route's bounded staging pool, engine.hpp:56-58):
+//   the segment's logical window [lo, hi) wraps onto its physical buffer [phys, phys + ring),
+//   lap = (addr - lo) / ring. A CONSUME read of lap k waits for flags[g] >= k + 1 and,
+//   when it completes OK, stores its lap count into credits[g]; a PRODUCE write of lap k waits for
+//   credits[g] >= k (the consumer drained lap k - 1 of the granule).
 struct GateDev {
-  uint64_t lo, hi;         // device-usable address range of the segment
+  uint64_t lo, hi;         // device-usable address range of the segment (logical for a ring)
   uint32_t* flags;         // per-granule counters (written by the producing engine)
   uint32_t* consumed;      // per-granule consumption counters (CONSUME only, local HBM)
   uint32_t* produced;      // per-granule production counters (PRODUCE only, local HBM): the
                            // flag is written as a plain value, so it may live in any memory
                            // this GPU can store to (peer HBM, mapped pinned host memory)
+  uint32_t* credits;       // ring only: per-granule drained laps (CONSUME adds, PRODUCE waits)
+  uint64_t ring;           // physical bytes of a ring gate, 0 for a plain gate
+  uint64_t phys;           // ring only: device address of the physical buffer; lo is a tagged
+                           // virtual base (bit 63 set) that no real allocation can alias
   uint32_t role;
-  uint32_t pad_;
+  uint32_t ngran;          // granules of the physical buffer
 };
 
 // 2-hop relay rail (executor "relay", via GPU K). Hop 1: this engine's copy workers move a

@@ -876,7 +876,13 @@ void Engine::attach_board(void* board, uint32_t n_slots, uint32_t slot, uint64_t
 
 // ------------------------------------------------------------------ dataflow gates
 
-void Engine::gate_segment(const std::string& seg_id, uint32_t role, void* flags) {
+// logical_bytes != 0 makes a ring gate (the staged route's bounded staging pool,
+// reference engine.hpp:56-58 / engine.cpp:465-610): the segment's single buffer is the
+// physical ring, intents address a logical window of logical_bytes that wraps onto it, and
+// `credits` (one uint32 per granule, zeroed, shared by both ends) carries the consumer's
+// drained laps back to the producer.
+void Engine::gate_segment(const std::string& seg_id, uint32_t role, void* flags, void* credits,
+                          uint64_t logical_bytes) {
   std::lock_guard<std::mutex> lk(mu_);
   if (!started_) throw EngineError("engine not started");
   if (role != kGateConsume && role != kGateProduce) throw ConfigError("gate role must be consume (1) or produce (2)");
@@ -901,13 +907,31 @@ void Engine::gate_segment(const std::string& seg_id, uint32_t role, void* flags)
     ctl_->stop = 0;
     ctl_->state = 0;
   }
-  const Buffer& bf = s.seg.buffers.front();
+  Buffer& bf = s.seg.buffers.front();
   const uint64_t granules = (bf.length + opts_.chunk_bytes - 1) / opts_.chunk_bytes;
+  if (logical_bytes) {
+    if (!credits) throw ConfigError("ring gate: credits array is null");
+    if (bf.offset != 0 || bf.length % opts_.chunk_bytes)
+      throw ConfigError("ring gate: the ring buffer must start at offset 0 and be a multiple of b200.chunk_bytes");
+    if (logical_bytes < bf.length) throw ConfigError("ring gate: logical_bytes is smaller than the ring");
+    if (logical_bytes / bf.length >= (1ull << 32)) throw ConfigError("ring gate: too many laps");
+    if (E_.n_relays) throw ConfigError("ring gates are served by direct SM rails only (the fabric has relay rails)");
+  }
+  if (logical_bytes >= (1ull << 56)) throw ConfigError("ring gate: logical_bytes must stay below 2^56");
   GateDev g{};
   g.lo = bf.dev_addr;
-  g.hi = bf.dev_addr + bf.length;
+  if (logical_bytes) {
+    // the logical window gets a tagged virtual base of its own (bit 63 + the gate index):
+    // it can never alias a real allocation, and only this engine's workers, which wrap it
+    // onto the ring before touching memory, ever see it
+    g.phys = bf.dev_addr;
+    g.lo = (1ull << 63) | (uint64_t(E_.n_gates + 1) << 56);
+  }
+  g.hi = g.lo + (logical_bytes ? logical_bytes : bf.length);
   g.flags = static_cast<uint32_t*>(flags);
   g.role = role;
+  g.ring = logical_bytes ? bf.length : 0;
+  g.ngran = static_cast<uint32_t>(granules);
   {  // this engine's own per-granule counters (consumed or produced), zeroed
     CK(cudaSetDevice(device_));
     void* p = nullptr;
@@ -924,6 +948,16 @@ void Engine::gate_segment(const std::string& seg_id, uint32_t role, void* flags)
     if (cudaPointerGetAttributes(&pa, flags) == cudaSuccess && pa.type == cudaMemoryTypeHost && pa.devicePointer)
       g.flags = static_cast<uint32_t*>(pa.devicePointer);
     cudaGetLastError();
+  }
+  if (logical_bytes) {
+    g.credits = static_cast<uint32_t*>(credits);
+    cudaPointerAttributes pa{};
+    if (cudaPointerGetAttributes(&pa, credits) == cudaSuccess && pa.type == cudaMemoryTypeHost && pa.devicePointer)
+      g.credits = static_cast<uint32_t*>(pa.devicePointer);
+    cudaGetLastError();
+    s.ring = bf.length;
+    bf.length = logical_bytes;  // intents address the logical window; workers wrap onto the ring
+    bf.dev_addr = g.lo;
   }
   E_.gates[E_.n_gates++] = g;
   s.gated = true;
@@ -1036,6 +1070,8 @@ Intent Engine::make_intent(uint64_t batch, const spray_transfer_request& req, ui
   if (!ds.seg.covering(req.dst_offset, req.length))
     throw InvalidRangeError("destination range not covered by one registered buffer");
   const Direction dir = req.direction == SPRAY_READ ? Direction::kRead : Direction::kWrite;
+  if ((ss.ring && req.length > ss.ring) || (ds.ring && req.length > ds.ring))
+    throw InvalidRangeError("ring-gated segment: a transfer may not exceed the ring");
   if (ss.gated || ds.gated) {  // gated segments: every chunk is exactly one granule
     const uint64_t cb = opts_.chunk_bytes;
     uint64_t nsl = req.length / opts_.sched.min_slice_size;

@@ -108,7 +108,8 @@ class Engine {
   // Dataflow gate on a registered single-buffer segment (role kGateConsume/kGateProduce);
   // `flags` = one uint32 counter per chunk_bytes granule, device memory reachable from this
   // GPU (the producer's and the consumer's engines share it).
-  void gate_segment(const std::string& seg_id, uint32_t role, void* flags);
+  void gate_segment(const std::string& seg_id, uint32_t role, void* flags, void* credits = nullptr,
+                    uint64_t logical_bytes = 0);
   // GlobalLoadBoard (scheduler.hpp:66-90): publish/blend through a shared host board
   void attach_board(void* board, uint32_t n_slots, uint32_t slot, uint64_t period_ns);
   // prepared intents in one drain-mode launch, timed by CUDA events around the kernel only
@@ -128,6 +129,7 @@ class Engine {
     Segment seg;
     bool translated = false;
     bool gated = false;             // a dataflow gate covers this segment
+    uint64_t ring = 0;              // ring gate: physical bytes behind the logical window
     std::vector<void*> registered;  // host buffers we cudaHostRegister'ed
   };
 

@@ -9,6 +9,7 @@ from __future__ import annotations
 
 import ctypes as C
 import enum
+import time
 from dataclasses import dataclass, field
 from typing import List, Optional, Sequence
 
@@ -308,6 +309,14 @@ class Engine:
         counter per chunk_bytes() granule, shared by the producing and consuming engines."""
         _check(lib.spray_gate_segment(self._h, segment_id.encode(), int(role), flags_ptr))
 
+    def gate_ring(self, segment_id: str, role: int, flags_ptr: int, credits_ptr: int, logical_bytes: int):
+        """Ring gate (the staged route's bounded staging pool, engine.hpp:56-58): the
+        segment's single buffer is a ring that intents address through a logical window of
+        `logical_bytes` (lap = offset // ring). `flags_ptr` / `credits_ptr`: one zeroed uint32
+        per granule each, shared by both engines. See spray_gate_ring in include/spray_b200.h."""
+        _check(lib.spray_gate_ring(self._h, segment_id.encode(), int(role), flags_ptr, credits_ptr,
+                                   int(logical_bytes)))
+
     def telemetry_csv(self) -> str:
         """TelemetrySnapshot::to_csv columns from the device telemetry windows."""
         n = C.c_size_t()
@@ -550,3 +559,108 @@ def ipc_open(device: int, handle: bytes) -> int:
 
 def ipc_close(ptr: int):
     _check(lib.spray_ipc_close(ptr))
+
+
+class StagedRoute:
+    """Staged multi-hop route through a bounded pinned-host staging ring (SURVEY.md §8(f)
+    rank 1; reference `build_staged_exec` / `staged_try_start_chunks`, engine.cpp:465-527,
+    with `staging_chunk_bytes` 4 MiB and `staging_ring_depth` 4, engine.hpp:56-58).
+
+    The producer engine moves src -> ring and the consumer engine ring -> dst; a ring gate
+    (spray_gate_ring) pipelines them granule by granule on the device, so at most
+    `depth` chunks of the transfer occupy the pool and the host only writes intents. The
+    two engines may sit on different GPUs without peer access: the ring, its flags and
+    its credits live in mapped pinned host memory. Register while both engines are idle.
+    """
+
+    def __init__(self, producer: "Engine", consumer: "Engine", producer_node: str, consumer_node: str,
+                 chunk_bytes: int = 4 << 20, depth: int = 4, seg_id: str = "staged/ring",
+                 max_laps: int = 1 << 24):
+        cb = producer.chunk_bytes()
+        if consumer.chunk_bytes() != cb:
+            raise ConfigError("staged route: both engines need the same b200.chunk_bytes")
+        if chunk_bytes % cb or depth < 1:
+            raise ConfigError("staged route: chunk_bytes must be a multiple of b200.chunk_bytes, depth >= 1")
+        self.producer, self.consumer = producer, consumer
+        self.seg_id, self.chunk, self.granule = seg_id, chunk_bytes, cb
+        self.ring_bytes = chunk_bytes * depth
+        granules = self.ring_bytes // cb
+        self._ring = host_alloc(self.ring_bytes)
+        self._ctl = host_alloc(8 * granules)  # flags then credits, one uint32 per granule each
+        C.memset(self._ctl, 0, 8 * granules)
+        flags, credits = self._ctl, self._ctl + 4 * granules
+        self._credits = np.ctypeslib.as_array((C.c_uint32 * granules).from_address(credits))
+        for eng, node in ((producer, producer_node), (consumer, consumer_node)):
+            eng.register_segment(SegmentDescriptor(seg_id, Medium.HOST, node,
+                                                   [BufferDesc(0, self.ring_bytes, self._ring)]))
+        logical = self.ring_bytes * max_laps
+        producer.gate_ring(seg_id, Engine.GATE_PRODUCE, flags, credits, logical)
+        consumer.gate_ring(seg_id, Engine.GATE_CONSUME, flags, credits, logical)
+        self.logical_bytes = logical
+        self.cursor = 0  # next logical ring offset (monotonic: the lap is cursor // ring_bytes)
+
+    def transfer(self, src_segment: str, src_offset: int, dst_segment: str, dst_offset: int, length: int,
+                 timeout_s: float = 60.0) -> BatchState:
+        """Move src[src_offset:+length] -> dst[dst_offset:+length] through the ring as
+        `chunk_bytes` pieces (the reference's staged chunks): one consumer intent and one
+        producer intent per piece. Offsets must be multiples of b200.chunk_bytes. Blocks
+        until both ends finish; returns COMPLETE or FAILED.
+
+        Like `staged_try_start_chunks` (engine.cpp:506-527), at most `depth` pieces are
+        ahead of the consumer: a piece that reuses a ring slot is queued only once the
+        consumer's credits show the slot's previous lap drained (the credits sit in host
+        memory, so this poll costs no PCIe traffic). Neither engine's device pipeline then
+        holds work that waits on the other side. Pieces go into the engines' batches; a
+        batch that drained between two pieces is replaced by a fresh one (a completed
+        batch takes no more intents, engine.cpp:239-253)."""
+        if length <= 0:
+            raise InvalidRangeError("zero-length transfer")
+        if self.cursor + length > self.logical_bytes:
+            raise InvalidRangeError("staged route: logical ring window exhausted")
+        batches = {self.producer: [], self.consumer: []}
+
+        def put(eng, req):
+            for _ in range(2):
+                if not batches[eng]:
+                    batches[eng].append(eng.allocate_batch())
+                try:
+                    eng.submit_transfer(batches[eng][-1], req)
+                    return
+                except EngineError as e:
+                    if "already complete" not in str(e):
+                        raise
+                    batches[eng].append(eng.allocate_batch())
+            raise EngineError("staged route: could not queue a piece")
+
+        pos = 0
+        deadline = time.monotonic() + timeout_s
+        while pos < length:
+            n = min(self.chunk, length - pos)
+            c = self.cursor
+            lap, g0 = divmod(c, self.ring_bytes)
+            g0 //= self.granule
+            ng = -(-n // self.granule)
+            while lap and int(self._credits[g0:g0 + ng].min()) < lap:
+                if time.monotonic() > deadline:
+                    raise EngineError("staged route: the consumer did not drain the ring in time")
+                time.sleep(10e-6)
+            put(self.consumer, TransferRequest(self.seg_id, c, dst_segment, dst_offset + pos, n))
+            put(self.producer, TransferRequest(src_segment, src_offset + pos, self.seg_id, c, n))
+            self.cursor += ng * self.granule
+            pos += n
+        state = BatchState.COMPLETE
+        rem_ns = max(1, int((deadline - time.monotonic()) * 1e9))
+        for eng in (self.producer, self.consumer):
+            for b in batches[eng]:
+                st = eng.await_batch(b, rem_ns)
+                if st.state != BatchState.COMPLETE:
+                    state = BatchState.FAILED
+                eng.free_batch(b)
+        return state
+
+    def close(self):
+        """Free the ring once both engines are stopped."""
+        if self._ring:
+            host_free(self._ring)
+            host_free(self._ctl)
+            self._ring = self._ctl = 0

@@ -501,6 +501,45 @@ def test_staged_route_through_host_memory_bit_exact():
     sp.host_free(flags_p)
 
 
+def test_staged_ring_route_bounded_pool_bit_exact():
+    """Staged route through a BOUNDED staging pool (reference staged_* pipeline,
+    engine.cpp:465-527; 4 MiB chunks x ring depth 4, engine.hpp:56-58): 192 MiB moves
+    HBM -> 16 MiB pinned-host ring -> HBM, 12 laps, in two transfers that continue the
+    ring's lap count. Every byte arrives; every granule's credit equals its laps; a
+    transfer larger than the ring and a misaligned offset are rejected like the reference's
+    InvalidRangeError."""
+    topo = fabrics.kv_offload(DEV)
+    cfg = {"resilience": {"degradation_ratio": 1e9}, "b200": {"chunk_bytes": 65536, "gate_timeout_ms": 20000}}
+    a, b = make_engine(topo, cfg), make_engine(topo, cfg)
+    n = 96 << 20
+    src, dst = dev_buf(n, 91), dev_buf(n)
+    node = f"g{DEV}"
+    for e in (a, b):
+        e.register_segment(sp.SegmentDescriptor("src", sp.Medium.DEVICE, node, [sp.BufferDesc(0, n, src.data_ptr())]))
+        e.register_segment(sp.SegmentDescriptor("dst", sp.Medium.DEVICE, node, [sp.BufferDesc(0, n, dst.data_ptr())]))
+    route = sp.StagedRoute(a, b, node, node, chunk_bytes=4 << 20, depth=4)
+    assert route.ring_bytes == 16 << 20
+    granules = route.ring_bytes // a.chunk_bytes()
+    ctl = np.ctypeslib.as_array((C.c_uint32 * (2 * granules)).from_address(route._ctl))
+    for run in range(2):
+        dst.zero_()
+        torch.cuda.synchronize()
+        assert route.transfer("src", 0, "dst", 0, n) == sp.BatchState.COMPLETE
+        assert torch.equal(src, dst), run
+        laps = (run + 1) * n // route.ring_bytes
+        assert int(ctl[:granules].min()) == laps and int(ctl[:granules].max()) == laps  # flags
+        assert int(ctl[granules:].min()) == laps and int(ctl[granules:].max()) == laps  # credits
+    ba = a.allocate_batch()
+    with pytest.raises(sp.InvalidRangeError):
+        a.submit_transfer(ba, sp.TransferRequest("src", 0, route.seg_id, route.cursor, route.ring_bytes + (64 << 10)))
+    with pytest.raises(sp.InvalidRangeError):
+        a.submit_transfer(ba, sp.TransferRequest("src", 4096, route.seg_id, route.cursor, 1 << 20))
+    a.free_batch(ba)
+    a.stop()
+    b.stop()
+    route.close()
+
+
 def test_telemetry_csv_windows_account_every_byte():
     """TelemetrySnapshot::to_csv columns (telemetry.cpp:123-158) from the device window
     cells: per-window bytes sum to the delivered bytes, per rail; percentiles ordered."""
