@@ -598,6 +598,7 @@ class StagedRoute:
         consumer.gate_ring(seg_id, Engine.GATE_CONSUME, flags, credits, logical)
         self.logical_bytes = logical
         self.cursor = 0  # next logical ring offset (monotonic: the lap is cursor // ring_bytes)
+        self.stats = {"wait_s": 0.0, "submit_s": 0.0, "pieces": 0}  # host time of transfer()
 
     def transfer(self, src_segment: str, src_offset: int, dst_segment: str, dst_offset: int, length: int,
                  timeout_s: float = 60.0) -> BatchState:
@@ -640,12 +641,17 @@ class StagedRoute:
             lap, g0 = divmod(c, self.ring_bytes)
             g0 //= self.granule
             ng = -(-n // self.granule)
+            t0 = time.perf_counter()
             while lap and int(self._credits[g0:g0 + ng].min()) < lap:
                 if time.monotonic() > deadline:
                     raise EngineError("staged route: the consumer did not drain the ring in time")
                 time.sleep(10e-6)
+            t1 = time.perf_counter()
             put(self.consumer, TransferRequest(self.seg_id, c, dst_segment, dst_offset + pos, n))
             put(self.producer, TransferRequest(src_segment, src_offset + pos, self.seg_id, c, n))
+            self.stats["wait_s"] += t1 - t0
+            self.stats["submit_s"] += time.perf_counter() - t1
+            self.stats["pieces"] += 1
             self.cursor += ng * self.granule
             pos += n
         state = BatchState.COMPLETE

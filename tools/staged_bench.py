@@ -54,6 +54,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--mib", type=int, default=1024)
     ap.add_argument("--depth", type=int, default=4)
+    ap.add_argument("--chunk-mib", type=int, default=4)
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--gpus", type=int, default=1)
     o = ap.parse_args()
@@ -67,7 +68,7 @@ def main():
 
     a, b = engines(gp, gc)
     register(a, b, gp, gc, src, dst, n)
-    route = sp.StagedRoute(a, b, f"g{gp}", f"g{gc}", chunk_bytes=4 << 20, depth=o.depth)
+    route = sp.StagedRoute(a, b, f"g{gp}", f"g{gc}", chunk_bytes=o.chunk_mib << 20, depth=o.depth)
     t = None
     for _ in range(o.reps):
         torch.cuda.synchronize()
@@ -78,8 +79,11 @@ def main():
         t = w if t is None else min(t, w)
     torch.cuda.synchronize(gc)
     ok = torch.equal(src.cpu(), dst.cpu())
+    st = route.stats
     out["ring"] = {"pool_bytes": route.ring_bytes, "chunk_bytes": route.chunk, "depth": o.depth,
-                   "gbs": round(n / t / 1e9, 2), "ms": round(t * 1e3, 2), "bit_exact": ok}
+                   "gbs": round(n / t / 1e9, 2), "ms": round(t * 1e3, 2), "bit_exact": ok,
+                   "host_us_per_piece": {"credit_wait": round(st["wait_s"] / st["pieces"] * 1e6, 1),
+                                         "submit": round(st["submit_s"] / st["pieces"] * 1e6, 1)}}
     a.stop()
     b.stop()
     route.close()
