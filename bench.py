@@ -659,7 +659,9 @@ def run_b200(args):
         except Exception:
             pass
         traffic = None
-        prof = os.path.join(ROOT, "profiles", "ncu_engine_kernel.json")
+        prof = os.path.join(ROOT, "profiles", "ncu_engine_kernel_final_r01.json")
+        if not os.path.exists(prof):
+            prof = os.path.join(ROOT, "profiles", "ncu_engine_kernel.json")
         if os.path.exists(prof):
             try:
                 traffic = json.load(open(prof)).get("dram_bytes_per_launch")
@@ -681,7 +683,7 @@ def run_b200(args):
                     "h2d_bytes_per_step": pool_bytes + 64 * 2 * nb, "d2h_bytes_per_step": pool_bytes + 16},
             "roofline": {"bound": "pcie", "achieved": round(per_launch_gbs, 3), "peak": peak, "unit": "GB/s",
                          "frac": round(per_launch_gbs / peak, 4), "traffic": traffic,
-                         "traffic_unit": "DRAM bytes per launch (ncu, profiles/ncu_engine_kernel.json); the "
+                         "traffic_unit": "DRAM bytes per launch (ncu, " + os.path.relpath(prof, ROOT) + "); the "
                                          "host-link bytes per launch there equal the algorithmic 512 MiB",
                          "peak_source": peak_src, "nominal_gbs": 2 * PCIE_NOMINAL_GBS,
                          "sm_copy_ceiling_gbs": link.get("sm_both_lsu_gbs", 80.35),
