@@ -166,6 +166,20 @@ int spray_engine_counters(spray_engine* e, uint64_t* bytes_dispatched, uint64_t*
  * (sim_backend.cpp:188-200 semantics). */
 int spray_inject_fault(spray_engine* e, const char* rail_id, int32_t effect, uint64_t start_ns,
                        uint64_t end_ns, double factor);
+/* spray::FaultEntry (backend.hpp:79-86) in full: effect DOWN / DEGRADE (factor in (0, 1]) /
+ * JITTER (uniform added delay in [0, jitter_us) per copy unit, sim_backend.cpp:48-61) /
+ * DROP_COMPLETION (the bytes land, the completion is lost; the attempt times out after
+ * resilience.slice_timeout_ms and is retried, engine.cpp:996-1022). An entry replaces the
+ * rail's previous entry of the same effect (FaultSchedule::validate forbids overlaps per
+ * (rail, effect)). spray_inject_fault(e, r, JITTER, s, t, f) is this call with jitter_us = f. */
+typedef struct spray_fault_entry {
+  const char* rail_id;
+  int32_t effect;            /* enum spray_fault_effect */
+  uint64_t start_ns, end_ns; /* engine clock (spray_engine_now_ns) */
+  double factor;             /* degrade: effective bandwidth multiplier */
+  double jitter_us;          /* jitter: added uniform delay bound */
+} spray_fault_entry;
+int spray_inject_fault_entry(spray_engine* e, const spray_fault_entry* entry);
 int spray_clear_faults(spray_engine* e);
 uint64_t spray_engine_now_ns(spray_engine* e);
 

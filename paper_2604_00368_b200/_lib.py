@@ -46,6 +46,11 @@ class TransferRequestC(C.Structure):
                 ("dst_offset", C.c_uint64), ("length", C.c_uint64), ("direction", C.c_int32)]
 
 
+class FaultEntryC(C.Structure):  # spray_fault_entry (FaultEntry, backend.hpp:79-86)
+    _fields_ = [("rail_id", C.c_char_p), ("effect", C.c_int32), ("start_ns", C.c_uint64), ("end_ns", C.c_uint64),
+                ("factor", C.c_double), ("jitter_us", C.c_double)]
+
+
 class BatchStatusC(C.Structure):
     _fields_ = [("state", C.c_int32), ("remaining", C.c_uint64), ("failure_reason", C.c_char * 64)]
 
@@ -103,6 +108,7 @@ _SIGS = {
     "spray_rail_stats_get": (C.c_int, [P, C.c_uint32, C.POINTER(RailStatsC)]),
     "spray_engine_counters": (C.c_int, [P, U64P, U64P, U64P]),
     "spray_inject_fault": (C.c_int, [P, C.c_char_p, C.c_int32, C.c_uint64, C.c_uint64, C.c_double]),
+    "spray_inject_fault_entry": (C.c_int, [P, C.POINTER(FaultEntryC)]),
     "spray_clear_faults": (C.c_int, [P]),
     "spray_engine_now_ns": (C.c_uint64, [P]),
     "spray_heal_stats": (C.c_int, [P, U64P, U64P, U64P, U64P]),

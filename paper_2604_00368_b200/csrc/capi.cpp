@@ -143,7 +143,17 @@ int spray_engine_counters(spray_engine* e, uint64_t* d, uint64_t* t, uint64_t* f
   return guard([&] { e->eng->counters(d, t, f); });
 }
 int spray_inject_fault(spray_engine* e, const char* rail, int32_t effect, uint64_t start, uint64_t end, double factor) {
-  return guard([&] { e->eng->inject_fault(rail ? rail : "", effect, start, end, factor); });
+  return guard([&] {
+    e->eng->inject_fault(rail ? rail : "", effect, start, end, effect == SPRAY_FAULT_JITTER ? 1.0 : factor,
+                         effect == SPRAY_FAULT_JITTER ? factor : 0.0);
+  });
+}
+
+int spray_inject_fault_entry(spray_engine* e, const spray_fault_entry* f) {
+  return guard([&] {
+    if (!f) throw ConfigError("null fault entry");
+    e->eng->inject_fault(f->rail_id ? f->rail_id : "", f->effect, f->start_ns, f->end_ns, f->factor, f->jitter_us);
+  });
 }
 int spray_clear_faults(spray_engine* e) { return guard([&] { e->eng->clear_faults(); }); }
 uint64_t spray_engine_now_ns(spray_engine* e) { return e->eng->now_ns(); }
@@ -214,26 +224,12 @@ int spray_plan_candidates(spray_engine* e, const char* src, const char* dst, int
 int spray_prepare_transfers(spray_engine* e, const spray_transfer_request* reqs, size_t n, spray_prepared** out) {
   return guard([&] {
     CK(cudaSetDevice(e->eng->device()));  // callers may be on any thread / current device
-    // plan + validate through a scratch batch, exactly like submit_transfer
-    const uint64_t b = e->eng->allocate_batch();
-    std::vector<Intent> v(n);
     uint64_t slices = 0;
-    try {
-      for (size_t i = 0; i < n; ++i) {
-        uint64_t k = 0;
-        v[i] = e->eng->make_intent(b, reqs[i], &k);
-        slices += k;
-      }
-    } catch (...) {
-      e->eng->free_batch(b);
-      throw;
-    }
-    e->eng->free_batch(b);
+    const std::vector<Intent> v = e->eng->prepare(reqs, n, &slices);  // under the engine lock
     auto* p = new spray_prepared;
     p->owner = e;
     p->n = n;
     p->slices = slices;
-    CK(cudaSetDevice(e->eng->device()));
     CK(cudaMalloc(&p->dev, std::max<size_t>(1, n) * sizeof(Intent)));
     CK(cudaMemcpy(p->dev, v.data(), n * sizeof(Intent), cudaMemcpyHostToDevice));
     *out = p;
@@ -245,12 +241,15 @@ int spray_run_prepared(spray_engine* e, uint64_t batch, spray_prepared* p, float
     if (p->owner != e) throw EngineError("prepared set belongs to another engine");
     Engine& g = *e->eng;
     CK(cudaSetDevice(g.device()));  // events below belong to the engine's device
-    g.set_drain(true);
+    struct DrainGuard {  // drain mode is off again however the run ends
+      Engine& g;
+      explicit DrainGuard(Engine& e) : g(e) { g.set_drain(true); }
+      ~DrainGuard() { g.set_drain(false); }
+    } drain(g);
     // make sure no launch is resident, so this one is bracketed alone
     while (g.running_kernel()) std::this_thread::sleep_for(std::chrono::microseconds(50));
     CK(cudaStreamSynchronize(g.stream()));
     const float ms = g.run_device_intents_timed(batch, p->dev, p->n, p->slices);  // one drain-mode launch
-    g.set_drain(false);
     if (kernel_ms) *kernel_ms = ms;
   });
 }

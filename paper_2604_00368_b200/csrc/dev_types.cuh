@@ -32,6 +32,9 @@ struct RailDesc {
   uint32_t ce_index;      // CE proxy stream index (CE rails); relay index (relay rails)
   uint8_t n_partners;     // probe counterparts, affinity partner first (resilience.cpp:17-44)
   uint8_t partners[15];
+  uint32_t window;        // posting window: units (chunks; CE orders) in flight on the rail
+                          // (SimBackend inflight_window, sim_backend.cpp:81; engine.cpp:884-948)
+  uint32_t pad_w;
 };
 
 // Scheduler cost state (scheduler.hpp:158-168) + resilience record (resilience.hpp:68-76)
@@ -95,11 +98,12 @@ struct Slice {
   uint32_t batch_slot;
   uint32_t set_id;
   uint32_t model;          // 1 = dispatched by the cost model
-  uint32_t target;         // slot chunk counter value once this attempt's chunks are done
+  uint32_t target;         // units (chunks; 1 for a CE order) of the current attempt
   uint32_t n_failed_pairs;
   uint8_t failed_local[4], failed_remote[4];  // burned pairs (engine.cpp:765-767)
   uint32_t kind;           // kSliceData or kSliceProbe (engine.hpp:133 SliceKind)
-  uint8_t pad_[20];
+  uint32_t gen;            // attempt generation of the slot's counter (last issued attempt)
+  uint8_t pad_[16];
 };
 constexpr uint32_t kSliceData = 0, kSliceProbe = 2;
 static_assert(sizeof(Slice) == 128, "slice record is 128 B");
@@ -110,17 +114,32 @@ struct WorkItem {
   uint64_t src, dst;
   uint32_t len;
   uint32_t slice;
-  uint32_t target;         // completion when the slot's chunk counter reaches this
+  uint32_t target;         // units of the attempt: its slot counter closes at this count
   uint16_t rail, remote;   // fault words to honour (remote 0xffff = none)
-  uint32_t attempt;
+  uint32_t gen;            // attempt generation (slot counter high word)
   uint32_t pad_;
   uint32_t stamp;
   uint32_t pad2_;
 };
 static_assert(sizeof(WorkItem) == 48, "work item is 48 B");
 static_assert(offsetof(WorkItem, len) == 16 && offsetof(WorkItem, rail) == 28 && offsetof(WorkItem, remote) == 30 &&
-                  offsetof(WorkItem, attempt) == 32 && offsetof(WorkItem, stamp) == 40,
-              "EGRESS writes work items as two 16-byte vectors + the attempt word");
+                  offsetof(WorkItem, gen) == 32 && offsetof(WorkItem, stamp) == 40,
+              "EGRESS writes work items as two 16-byte vectors + the generation word");
+
+// Per-slot attempt counter (HBM, one 64-bit word per slice slot): the exactly-once rule of
+// process_completion (engine.cpp:792-797: an event for an attempt that is no longer
+// outstanding is stale) on the device. high 32 bits = the attempt generation EGRESS armed it
+// with; bits 29..0 = units of that attempt delivered; FAIL = some unit failed; CLOSED = the
+// attempt's terminal event is decided. Units count only while the generation matches and
+// the word is open, so a late unit of a timed-out attempt never counts for its retry, and
+// exactly one of {the last unit, the timeout scanner} closes an attempt and posts its
+// completion word.
+constexpr uint64_t kCtrClosed = 1ull << 31, kCtrFail = 1ull << 30, kCtrCount = (1ull << 30) - 1;
+
+// Posting deadline of the outstanding attempt of a slot (worker_timeout_phase analog,
+// engine.cpp:953-956, 996-1022): bits 47..0 = (engine ns >> 10) after which the attempt
+// times out, bits 63..48 = low 16 bits of its generation; 0 = none.
+constexpr uint64_t kDlMask = (1ull << 48) - 1;
 
 // Device completion word: one 8-byte store carries slice, status and the publication
 // stamp, so a reader validates and reads it in a single access (no acquire fence).
@@ -131,7 +150,7 @@ __host__ __device__ inline uint64_t pack_completion(uint32_t slice, uint32_t sta
 // Completion record posted by the CE proxy on the host (mapped ring). 32 B.
 struct Completion {
   uint32_t slice;
-  uint32_t attempt;
+  uint32_t gen;            // attempt generation of the order
   uint32_t status;
   uint32_t rail;
   uint64_t t_done;         // engine clock at completion
@@ -142,8 +161,8 @@ struct Completion {
 // CE work order to the host proxy (mapped host ring), 48 B.
 struct CeOrder {
   uint64_t src, dst, len;
-  uint32_t slice, attempt;
-  uint32_t rail, ce_index;
+  uint32_t slice, gen;     // slot and attempt generation (echoed in the Completion)
+  uint32_t rail, remote;   // fault words the proxy honours (remote 0xffffffff = none)
   uint64_t stamp;
 };
 
@@ -153,14 +172,20 @@ struct CeOrder {
 struct BatchDev {
   uint64_t done;           // slices delivered through this slot (finish_logical count)
   uint64_t failed_id;      // batch id that failed terminally in this slot (0 = none)
+  uint64_t owner;          // HBM copy only: newest batch id whose slices used this slot;
+                           // a completion of an older batch id is from a freed failed batch
+  uint64_t pad_;
 };
 
-// Fault word per rail (FaultSchedule entry, backend.hpp:74-94).
+// Fault words per rail: one FaultEntry (backend.hpp:74-94) per effect, as the reference
+// schedule allows one interval per (rail, effect) (FaultSchedule::validate).
+enum : uint32_t { kFxDown = 0, kFxDegrade = 1, kFxJitter = 2, kFxDrop = 3 };
 struct FaultDev {
-  uint64_t start, end;     // engine ns
-  uint32_t effect;         // 0 down, 1 degrade, 2 jitter, 3 drop
-  uint32_t active;
-  double factor;
+  uint64_t start[4], end[4];  // engine ns, per effect
+  double factor;              // degrade: bandwidth multiplier
+  double jitter_us;           // jitter: uniform added delay bound (FaultEntry::jitter_us)
+  uint32_t active;            // bit e: effect e scheduled (written last)
+  uint32_t pad_;
 };
 
 // The host<->device control block (mapped host memory). The first 32 bytes are the
@@ -246,7 +271,7 @@ struct GateDev {
 constexpr int kMaxRelays = 8;
 struct RelayDesc {  // 32 B, in K's HBM: written by the hop-1 worker, read by the forwarder
   uint64_t dst;
-  uint32_t len, slice, target, pad_;
+  uint32_t len, slice, target, gen;  // target = units of the attempt, gen = its generation
   uint64_t stamp;   // (launch_gen << 32) | (ticket + 1), release-stored last
 };
 struct RelayDev {
@@ -292,9 +317,11 @@ struct EngineDev {
   RailState* rail_state;                       // HBM (persisted between launches)
   const CandSet* sets; uint32_t n_sets;        // HBM
   Slice* slices; uint32_t n_slices;            // HBM
-  uint64_t* free_slices;                       // HBM stack of (slot | chunk-counter base << 32)
-  uint32_t* slot_done;                         // HBM per-slot chunk counters (workers, monotonic)
-  uint32_t* slot_fail;                         // HBM per-slot failed-attempt target (workers)
+  uint64_t* free_slices;                       // HBM stack of (slot | last attempt generation << 32)
+  unsigned long long* slot_ctr;                // HBM per-slot attempt counters (see kCtrClosed)
+  unsigned long long* deadline;                // HBM per-slot posting deadline (see kDlMask)
+  uint32_t* pending;                           // HBM [n_rails][n_slices]: decided, not yet posted
+  uint64_t* pend_pos;                          // HBM [2][kMaxRails]: pending head / tail per rail
   WorkItem* work; uint64_t work_cap;           // HBM MPMC ring
   unsigned long long* work_head;               // HBM ticket counter (workers)
   uint64_t* comp; uint64_t comp_cap;           // HBM MPSC ring of packed completion words
@@ -314,6 +341,10 @@ struct EngineDev {
   double degradation_ratio, degradation_min_t;
   uint32_t max_attempts;
   uint32_t has_ce;                             // poll the CE proxy completion ring
+  uint64_t slice_timeout_ns;                   // ResilienceConfig::slice_timeout (0 = none)
+  uint32_t fence_batch;                        // chunks a copy warp moves per system fence (1..4)
+  uint32_t pad_fb_;
+  uint64_t timeout_scan_ns;                    // deadline scan period of the TIMER warp
   uint64_t probe_interval, probe_bytes;        // resilience.hpp:23-26
   double probe_backoff_mult;
   int32_t probe_backoff_cap, pad_pb_;
@@ -339,6 +370,6 @@ struct EngineDev {
 
 // scalars persisted in EngineDev::persist between launches
 enum : int { kPRr = 0, kPWorkTail = 1, kPCompHead = 2, kPFreeTop = 3, kPParked = 4,
-             kPLastReset = 5, kPOutChunks = 6, kPOutSlices = 7, kPNum = 16 };
+             kPLastReset = 5, kPOutChunks = 6, kPOutSlices = 7, kPSlotHwm = 8, kPNum = 16 };
 
 }  // namespace spray_dev

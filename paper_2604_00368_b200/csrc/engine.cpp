@@ -175,8 +175,11 @@ EngineOptions engine_options_from_json(const std::string& text) {
     if (j.contains("b200")) {
       const Json& b = j.at("b200");
       reject_unknown(b, {"grid", "block", "chunk_bytes", "idle_exit_ms", "slice_capacity", "work_capacity",
-                         "sub_capacity", "batch_slots", "gate_timeout_ms"},
+                         "sub_capacity", "batch_slots", "gate_timeout_ms", "post_window", "fence_batch"},
                      "b200");
+      eo.post_window = static_cast<uint32_t>(b.number_or("post_window", eo.post_window));
+      eo.fence_batch = static_cast<uint32_t>(b.number_or("fence_batch", eo.fence_batch));
+      if (eo.fence_batch < 1 || eo.fence_batch > 4) throw ConfigError("b200.fence_batch must be in [1, 4]");
       if (b.contains("gate_timeout_ms"))
         eo.gate_timeout_ns = static_cast<uint64_t>(b.at("gate_timeout_ms").as_number() * 1e6);
       eo.grid = static_cast<int>(b.number_or("grid", eo.grid));
@@ -187,7 +190,9 @@ EngineOptions engine_options_from_json(const std::string& text) {
       eo.work_capacity = static_cast<uint64_t>(b.number_or("work_capacity", double(eo.work_capacity)));
       eo.sub_capacity = static_cast<uint64_t>(b.number_or("sub_capacity", double(eo.sub_capacity)));
       eo.batch_slots = static_cast<uint32_t>(b.number_or("batch_slots", eo.batch_slots));
-      if (eo.block % 32 || eo.block < 192 || eo.block > 1024) throw ConfigError("b200.block must be a multiple of 32 in [192, 1024]");
+      if (eo.block % 32 || eo.block < 256 || eo.block > 1024) throw ConfigError("b200.block must be a multiple of 32 in [256, 1024]");
+      if (eo.slice_capacity == 0 || eo.slice_capacity > (1u << 28))
+        throw ConfigError("b200.slice_capacity must be in [1, 2^28]");
       if (eo.chunk_bytes < 4096 || (eo.chunk_bytes & (eo.chunk_bytes - 1)) || eo.chunk_bytes > (1ull << 31))
         throw ConfigError("b200.chunk_bytes must be a power of two in [4096, 2^31]");
     }
@@ -272,7 +277,7 @@ void Engine::alloc_device() {
   bmirror_ = static_cast<BatchDev*>(host(sizeof(BatchDev) * opts_.batch_slots));
   faults_ = static_cast<FaultDev*>(host(sizeof(FaultDev) * kMaxRails));
   rmirror_ = static_cast<RailState*>(host(sizeof(RailState) * kMaxRails));
-  const uint64_t ce_cap = 4096, xc_cap = 1 << 16;
+  const uint64_t xc_cap = 1 << 16;
   ce_ring_ = static_cast<CeOrder*>(host(sizeof(CeOrder) * 8 * ce_cap));
   xc_ring_ = static_cast<Completion*>(host(sizeof(Completion) * xc_cap));
 
@@ -298,6 +303,15 @@ void Engine::alloc_device() {
   for (uint32_t i = 0; i < nr; ++i) {
     const RailDecl& r = topo_.rail(i);
     rd[i] = RailDesc{};
+    // posting window (SimBackend inflight_window, sim_backend.cpp:81): units in flight per
+    // rail. SM / relay rails: twice the worker warps, so one rail alone keeps every copy warp
+    // busy with a second chunk queued; CE rails: orders, at most half the proxy ring (the
+    // ring can then never overrun the proxy)
+    {
+      const uint32_t warps = static_cast<uint32_t>(std::max(1, launch_grid() - 1)) * (opts_.block / 32);
+      const uint32_t w = opts_.post_window ? opts_.post_window : (r.executor == 1 ? 2048u : std::max(64u, 2 * warps));
+      rd[i].window = r.executor == 1 ? std::min<uint32_t>(w, ce_cap / 2) : w;
+    }
     rd[i].bandwidth = r.bandwidth;
     rd[i].base_tier = r.tier;
     rd[i].id_rank = ranks[i];
@@ -358,8 +372,15 @@ void Engine::alloc_device() {
     CK(cudaMemcpyAsync(E_.free_slices, fl.data(), fl.size() * 8, cudaMemcpyHostToDevice, copy_stream_));
     CK(cudaStreamSynchronize(copy_stream_));
   }
-  E_.slot_done = static_cast<uint32_t*>(dev(sizeof(uint32_t) * opts_.slice_capacity));
-  E_.slot_fail = static_cast<uint32_t*>(dev(sizeof(uint32_t) * opts_.slice_capacity));
+  E_.slot_ctr = static_cast<unsigned long long*>(dev(sizeof(unsigned long long) * opts_.slice_capacity));
+  E_.deadline = static_cast<unsigned long long*>(dev(sizeof(unsigned long long) * opts_.slice_capacity));
+  E_.pending = static_cast<uint32_t*>(dev(sizeof(uint32_t) * opts_.slice_capacity * std::max<size_t>(1, nr)));
+  E_.pend_pos = static_cast<uint64_t*>(dev(sizeof(uint64_t) * 2 * kMaxRails));
+  E_.slice_timeout_ns = opts_.res.slice_timeout_ns;
+  E_.fence_batch = opts_.fence_batch;
+  // the deadline scan runs ~8 times per timeout (the reference's wheel has 10 ms buckets,
+  // engine.cpp:18), bounded to [0.2, 10] ms
+  E_.timeout_scan_ns = std::min<uint64_t>(10'000'000, std::max<uint64_t>(200'000, opts_.res.slice_timeout_ns / 8));
   E_.faults_hbm = static_cast<FaultDev*>(dev(sizeof(FaultDev) * kMaxRails));
   E_.next_free = static_cast<unsigned long long*>(dev(sizeof(unsigned long long) * kMaxRails));
   {  // telemetry windows: every cell starts empty (window = ~0)
@@ -570,8 +591,7 @@ void Engine::stop() {
 
 // ------------------------------------------------------------------ kernel lifecycle
 
-void Engine::launch() {
-  CK(cudaSetDevice(device_));
+int Engine::launch_grid() {
   int grid = opts_.grid;
   if (grid <= 0) {
     int sms = 0;
@@ -586,6 +606,12 @@ void Engine::launch() {
     for (RailIndex i = 0; i < topo_.rail_count(); ++i)
       if (topo_.rail(i).executor == 2 && topo_.rail(i).via == device_) grid = std::min(grid, sms - 16);
   }
+  return grid;
+}
+
+void Engine::launch() {
+  CK(cudaSetDevice(device_));
+  const int grid = launch_grid();
   ctl_->stop = 0;
   ctl_->drain = drain_ ? 1u : 0u;
   ctl_->state = 1;
@@ -973,6 +999,10 @@ Engine::BatchRec& Engine::batch_ref(uint64_t id) {
 
 uint64_t Engine::allocate_batch() {
   std::lock_guard<std::mutex> lk(mu_);
+  return allocate_batch_locked();
+}
+
+uint64_t Engine::allocate_batch_locked() {
   if (!started_) throw EngineError("engine not started");
   for (uint32_t k = 0; k < opts_.batch_slots; ++k) {
     const uint32_t slot = (next_slot_ + k) % opts_.batch_slots;
@@ -1026,6 +1056,10 @@ spray_batch_status_t Engine::await_batch(uint64_t batch, uint64_t limit_ns) {
 
 void Engine::free_batch(uint64_t batch) {
   std::lock_guard<std::mutex> lk(mu_);
+  free_batch_locked(batch);
+}
+
+void Engine::free_batch_locked(uint64_t batch) {
   BatchRec& b = batch_ref(batch);
   volatile BatchDev* m = &bmirror_[b.slot];
   const bool failed = m->failed_id == b.id;
@@ -1159,6 +1193,29 @@ size_t Engine::submit_transfers(uint64_t batch, const spray_transfer_request* re
   return done;
 }
 
+// Plans and validates n requests exactly like submit_transfer (through a scratch batch), under
+// the engine lock, and returns the intents for a device-resident submission.
+std::vector<Intent> Engine::prepare(const spray_transfer_request* reqs, size_t n, uint64_t* slices) {
+  std::lock_guard<std::mutex> lk(mu_);
+  const uint64_t b = allocate_batch_locked();
+  std::vector<Intent> v(n);
+  uint64_t total = 0;
+  try {
+    LookupCache lc;
+    for (size_t i = 0; i < n; ++i) {
+      uint64_t k = 0;
+      v[i] = make_intent(b, reqs[i], &k, &lc);
+      total += k;
+    }
+  } catch (...) {
+    free_batch_locked(b);
+    throw;
+  }
+  free_batch_locked(b);
+  *slices = total;
+  return v;
+}
+
 void Engine::submit_device_intents(uint64_t batch, const void* dev_intents, uint64_t n, uint64_t total_slices) {
   std::lock_guard<std::mutex> lk(mu_);
   BatchRec& b = batch_ref(batch);
@@ -1247,20 +1304,29 @@ void Engine::counters(uint64_t* d, uint64_t* t, uint64_t* f) {
   *f = ctl_->batches_failed;
 }
 
-void Engine::inject_fault(const std::string& rail, int effect, uint64_t start, uint64_t end, double factor) {
+// One FaultEntry (backend.hpp:79-86) applied to the live fabric; FaultSchedule::validate's
+// rules: a non-empty interval, a positive degrade factor, a non-negative jitter bound. An
+// entry replaces the rail's previous entry of the same effect.
+void Engine::inject_fault(const std::string& rail, int effect, uint64_t start, uint64_t end, double factor,
+                          double jitter_us) {
   std::lock_guard<std::mutex> lk(mu_);
   if (!started_) throw EngineError("engine not started");
   auto r = topo_.rail_index(rail);
   if (!r) throw ConfigError("fault schedule references unknown rail '" + rail + "'");
   if (end <= start) throw ConfigError("fault interval must be non-empty");
   if (effect < 0 || effect > 3) throw ConfigError("unknown fault effect");
-  if (effect != 0 && effect != 1) throw ConfigError("only down and degrade faults are emulated on hardware rails");
+  if (effect == kFxDegrade && !(factor > 0.0 && factor <= 1.0)) throw ConfigError("degrade factor must be in (0, 1]");
+  if (effect == kFxJitter && !(jitter_us >= 0.0)) throw ConfigError("jitter_us must be >= 0");
   volatile FaultDev* f = &faults_[*r];
-  f->start = start;
-  f->end = end;
-  f->effect = static_cast<uint32_t>(effect);
-  f->factor = factor;
-  f->active = 1;
+  const uint32_t bit = 1u << effect;
+  f->active = f->active & ~bit;  // retract the effect while its words change
+  std::atomic_thread_fence(std::memory_order_seq_cst);
+  f->start[effect] = start;
+  f->end[effect] = end;
+  if (effect == kFxDegrade) f->factor = factor;
+  if (effect == kFxJitter) f->jitter_us = jitter_us;
+  std::atomic_thread_fence(std::memory_order_seq_cst);
+  f->active = f->active | bit;
   std::atomic_thread_fence(std::memory_order_seq_cst);
   ctl_->fault_epoch = ctl_->fault_epoch + 1;
   ctl_->heal_fault_start = 0;
@@ -1371,12 +1437,22 @@ void Engine::ce_proxy_loop(int k) {
   std::deque<Group> fifo;
   std::vector<cudaEvent_t> pool;
   uint64_t head = ctl_->ce_head[k];
+  // fault words of a rail the proxy honours (host view of the same FaultEntry words)
+  auto fault_at = [&](uint32_t rail, uint32_t effect, uint64_t now) {
+    if (rail >= kMaxRails) return false;
+    const volatile FaultDev* f = &faults_[rail];
+    return ((f->active >> effect) & 1u) && f->start[effect] <= now && now < f->end[effect];
+  };
   auto post = [&](const CeOrder& o, uint32_t status) {
+    // DROP_COMPLETION (sim_backend.cpp:151-156): the bytes landed, the event is lost; the
+    // device's deadline scan times the attempt out
+    const uint64_t now = ctl_->device_now;
+    if (status == kStOk && (fault_at(o.rail, kFxDrop, now) || fault_at(o.remote, kFxDrop, now))) return;
     const uint64_t pos = xc_reserve_.fetch_add(1);
     while (pos - ctl_->xc_head >= E_.xc_cap) _mm_pause();
     volatile Completion* c = &xc_ring_[pos % E_.xc_cap];
     c->slice = o.slice;
-    c->attempt = o.attempt;
+    c->gen = o.gen;
     c->status = status;
     c->rail = o.rail;
     std::atomic_thread_fence(std::memory_order_release);
@@ -1428,13 +1504,12 @@ void Engine::ce_proxy_loop(int k) {
       volatile CeOrder* vo = &ce_ring_[k * E_.ce_cap + (head % E_.ce_cap)];
       if (vo->stamp != head + 1) break;
       CeOrder o;
-      o.src = vo->src; o.dst = vo->dst; o.len = vo->len; o.slice = vo->slice; o.attempt = vo->attempt;
-      o.rail = vo->rail; o.ce_index = vo->ce_index; o.stamp = vo->stamp;
+      o.src = vo->src; o.dst = vo->dst; o.len = vo->len; o.slice = vo->slice; o.gen = vo->gen;
+      o.rail = vo->rail; o.remote = vo->remote; o.stamp = vo->stamp;
       ++head;
       any = true;
-      const volatile FaultDev* f = &faults_[o.rail];
       const uint64_t now = ctl_->device_now;
-      if (f->active && f->effect == 0 && f->start <= now && now < f->end) {
+      if (fault_at(o.rail, kFxDown, now) || fault_at(o.remote, kFxDown, now)) {
         post(o, kStFailed);
         continue;
       }

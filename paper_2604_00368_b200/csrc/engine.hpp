@@ -42,6 +42,10 @@ struct EngineOptions {
   uint32_t max_sets = 1024;
   uint64_t gate_timeout_ns = 10'000'000'000ull;  // dataflow gate wait before an attempt fails
   uint64_t window_ns = 10'000'000;              // telemetry window (stats_window_ms)
+  uint32_t fence_batch = 4;                      // chunks a copy warp copies per system fence when
+                                                 // its next chunk is already queued (1 = every chunk)
+  uint32_t post_window = 0;                      // units in flight per rail (0: 2 x worker warps for
+                                                 // SM/relay rails, 2048 orders for CE rails)
 };
 
 // engine_options_from_json (engine.cpp:1199-1307): unknown keys rejected.
@@ -83,6 +87,7 @@ class Engine {
   spray_dev::Intent make_intent(uint64_t batch, const spray_transfer_request& req, uint64_t* n_slices,
                                 LookupCache* lc = nullptr);
   void submit_device_intents(uint64_t batch, const void* dev_intents, uint64_t n, uint64_t total_slices);
+  std::vector<spray_dev::Intent> prepare(const spray_transfer_request* reqs, size_t n, uint64_t* slices);
   void set_drain(bool on);
   cudaStream_t stream() const { return stream_; }
   bool running_kernel();
@@ -91,7 +96,8 @@ class Engine {
   uint32_t rail_count() const { return static_cast<uint32_t>(topo_.rail_count()); }
   void rail_stats(uint32_t rail, spray_rail_stats* out);
   void counters(uint64_t* dispatched, uint64_t* terminated, uint64_t* failed);
-  void inject_fault(const std::string& rail, int effect, uint64_t start, uint64_t end, double factor);
+  void inject_fault(const std::string& rail, int effect, uint64_t start, uint64_t end, double factor,
+                    double jitter_us = 0.0);
   void clear_faults();
   uint64_t now_ns();
   void heal_stats(uint64_t* fs, uint64_t* ok, uint64_t* fa, uint64_t* ro);
@@ -138,6 +144,7 @@ class Engine {
   void alloc_device();
   void free_device();
   void launch();
+  int launch_grid();
   void ensure_running();
   uint32_t set_for(const Segment& src, const Segment& dst, Direction dir);
   void translate(SegRec& s);
@@ -145,6 +152,8 @@ class Engine {
   SegRec& seg_lookup(const char* name, const char*& cname, SegRec*& crec);
   void ce_proxy_loop(int k);
   BatchRec& batch_ref(uint64_t id);
+  uint64_t allocate_batch_locked();
+  void free_batch_locked(uint64_t batch);
   uint64_t decompose_count(uint64_t len) const;
 
   EngineOptions opts_;
@@ -198,6 +207,7 @@ class Engine {
   void sync_relays();
   bool host_only_sm_ = false;  // every SM rail stages through pinned host memory
   static constexpr int kHostLinkCtas = 48;
+  static constexpr uint64_t ce_cap = 4096;  // CE orders per proxy stream ring
 };
 
 }  // namespace spray

@@ -286,8 +286,12 @@ class Engine:
         _check(lib.spray_engine_counters(self._h, C.byref(d), C.byref(t), C.byref(f)))
         return {"bytes_dispatched": d.value, "bytes_terminated": t.value, "batches_failed": f.value}
 
-    def inject_fault(self, rail_id: str, effect: FaultEffect, start_ns: int, end_ns: int, factor: float = 1.0):
-        _check(lib.spray_inject_fault(self._h, rail_id.encode(), int(effect), start_ns, end_ns, factor))
+    def inject_fault(self, rail_id: str, effect: FaultEffect, start_ns: int, end_ns: int, factor: float = 1.0,
+                     jitter_us: float = 0.0):
+        """One FaultEntry (backend.hpp:79-86): DOWN, DEGRADE (factor), JITTER (jitter_us) or
+        DROP_COMPLETION on `rail_id` over [start_ns, end_ns) of the engine clock."""
+        fe = L.FaultEntryC(rail_id.encode(), int(effect), int(start_ns), int(end_ns), float(factor), float(jitter_us))
+        _check(lib.spray_inject_fault_entry(self._h, C.byref(fe)))
 
     def clear_faults(self):
         _check(lib.spray_clear_faults(self._h))
