@@ -218,7 +218,7 @@ def batch_latency(sp, eng, reqs, n_batches, per_batch):
 def congestion(sp, fabrics, dev, hbm, host, nb, blk, perm, reps=4):
     """Telemetry spraying vs state-blind round robin (Policy::kRoundRobin, a25) on the same
     two SM rails of this GPU's PCIe root when one rail is congested: a DEGRADE fault
-    (sim_backend.cpp:171-181 semantics on the real fabric: FIFO service at factor x B)
+    (sim_backend.cpp:83-93 semantics on the real fabric: FIFO service at factor x B)
     throttles g.pcie1 to 10% for the whole run. Workload: the offload half of the KV batch.
     The cost model only (degradation exclusion off), so the difference is the scheduler's."""
     out = {"workload": f"{nb} x {blk >> 10} KiB offload HBM->pinned host per batch",

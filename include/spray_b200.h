@@ -163,11 +163,11 @@ int spray_engine_counters(spray_engine* e, uint64_t* bytes_dispatched, uint64_t*
 /* FaultSchedule entry (backend.hpp:74-94) applied to the live device fabric.
  * Times are engine-relative nanoseconds (spray_engine_now_ns). A DOWN fault aborts
  * in-flight slices with a partial prefix write and fails new ones
- * (sim_backend.cpp:188-200 semantics). */
+ * (sim_backend.cpp:100-112 semantics). */
 int spray_inject_fault(spray_engine* e, const char* rail_id, int32_t effect, uint64_t start_ns,
                        uint64_t end_ns, double factor);
 /* spray::FaultEntry (backend.hpp:79-86) in full: effect DOWN / DEGRADE (factor in (0, 1]) /
- * JITTER (uniform added delay in [0, jitter_us) per copy unit, sim_backend.cpp:48-61) /
+ * JITTER (uniform added delay in [0, jitter_us) per copy unit, sim_backend.cpp:52-63) /
  * DROP_COMPLETION (the bytes land, the completion is lost; the attempt times out after
  * resilience.slice_timeout_ms and is retried, engine.cpp:996-1022). An entry replaces the
  * rail's previous entry of the same effect (FaultSchedule::validate forbids overlaps per
@@ -280,9 +280,9 @@ int spray_plan_candidates(spray_engine* e, const char* src_segment, const char* 
  *   RESET_RAIL(rail, now=t_ns)         reset_rail                          (scheduler.cpp:242-247)
  *   EXPECT_HEALTH(rail, state=flags)   assertion: health(rail) == state
  *   DUE_PROBES(now=t_ns)               due_probes(now): excluded rails whose timer
- *                                      elapsed go to PROBING       (resilience.cpp:220-244)
+ *                                      elapsed go to PROBING       (resilience.cpp:129-153)
  *   PROBE_DONE(rail, len, status, now=now_ns)  release(rail,len); observe_probe(rail,
- *                                      status, now)                (resilience.cpp:191-212)
+ *                                      status, now)                (resilience.cpp:100-121)
  *   BOARD(rail, len=(int64) global queued bytes, now=now_ns)  the load board's
  *                                      global_queued(rail) seen by every later
  *                                      effective_queued(rail) until the next BOARD event

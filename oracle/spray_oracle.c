@@ -91,7 +91,7 @@ static int pen_ok(const spray_sched_config* c, int tier) {
   return tier >= 1 && tier <= 3 && c->penalty[tier - 1] > 0.0;
 }
 
-/* scheduler.cpp:337-364 */
+/* scheduler.cpp:34-61 */
 int so_sched_config_validate(const spray_sched_config* c) {
   if (c->min_slice_size < 4096) return -1;
   if (c->max_slices_per_transfer == 0) return -1;
@@ -255,13 +255,13 @@ void so_periodic_reset(so_sched* s, uint64_t now) {
 
 /* ------------------------------------------------------------- resilience */
 
-static uint64_t backoff_interval(const so_sched* s, int level) { /* resilience.cpp:214-218 */
+static uint64_t backoff_interval(const so_sched* s, int level) { /* resilience.cpp:123-127 */
   double mult = 1.0;
   for (int i = 0; i < level; ++i) mult *= s->rcfg.probe_backoff_mult;
   return (uint64_t)((double)s->rcfg.probe_interval_ns * mult);
 }
 
-static void so_exclude(so_sched* s, uint32_t rail, uint64_t now) { /* resilience.cpp:137-148 */
+static void so_exclude(so_sched* s, uint32_t rail, uint64_t now) { /* resilience.cpp:46-57 */
   if (s->rails[rail].health == SPRAY_EXCLUDED) return;
   s->rails[rail].health = SPRAY_EXCLUDED;
   so_res_rail* r = &s->res[rail];
@@ -272,7 +272,7 @@ static void so_exclude(so_sched* s, uint32_t rail, uint64_t now) { /* resilience
   s->exclusions++;
 }
 
-/* resilience.cpp:162-189 */
+/* resilience.cpp:71-98 */
 void so_observe(so_sched* s, uint32_t local, uint32_t remote, int status, double t_obs_s,
                 double predicted_s, uint64_t now) {
   if (status != SPRAY_SLICE_OK) {
@@ -300,7 +300,7 @@ void so_observe(so_sched* s, uint32_t local, uint32_t remote, int status, double
   }
 }
 
-/* resilience.cpp:150-160 reintegrate */
+/* resilience.cpp:59-69 reintegrate */
 static void so_reintegrate(so_sched* s, uint32_t rail, uint64_t now) {
   s->rails[rail].health = SPRAY_HEALTHY;
   so_reset_rail(s, rail, now);
@@ -311,7 +311,7 @@ static void so_reintegrate(so_sched* s, uint32_t rail, uint64_t now) {
   r->backoff = 0;
 }
 
-/* resilience.cpp:191-212 observe_probe */
+/* resilience.cpp:100-121 observe_probe */
 void so_observe_probe(so_sched* s, uint32_t rail, int status, uint64_t now) {
   so_res_rail* r = &s->res[rail];
   r->probe_inflight = 0;
@@ -330,7 +330,7 @@ void so_observe_probe(so_sched* s, uint32_t rail, int status, uint64_t now) {
   }
 }
 
-/* resilience.cpp:220-244 due_probes (the partner choice does not touch scheduler state) */
+/* resilience.cpp:129-153 due_probes (the partner choice does not touch scheduler state) */
 void so_due_probes(so_sched* s, uint64_t now) {
   for (uint32_t i = 0; i < s->n_rails; ++i) {
     const int h = s->rails[i].health;
@@ -501,7 +501,7 @@ int so_hist_bucket(uint64_t t) {
 
 static uint64_t from_seconds(double s) { return (uint64_t)(s * 1e9); } /* common.hpp:21 */
 
-/* sim_backend.cpp:171-181 */
+/* sim_backend.cpp:83-93 */
 uint64_t so_sim_done_ns(uint64_t now, uint64_t next_free, uint64_t len, double bw,
                         double service_factor, double degrade, double latency_us) {
   const uint64_t start = now > next_free ? now : next_free;
@@ -511,7 +511,7 @@ uint64_t so_sim_done_ns(uint64_t now, uint64_t next_free, uint64_t len, double b
   return start + from_seconds(latency_us * 1e-6) + from_seconds(service_s) + from_seconds(0.0 * 1e-6);
 }
 
-/* sim_backend.cpp:192-200 */
+/* sim_backend.cpp:104-112 */
 uint64_t so_sim_partial_bytes(uint64_t len, uint64_t start, uint64_t done, uint64_t down_start) {
   if (down_start <= start) return 0;
   const double frac = (double)(down_start - start) / (double)(done - start);

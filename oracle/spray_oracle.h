@@ -43,7 +43,7 @@ uint64_t so_checksum(const uint8_t* p, uint64_t n);
 uint64_t so_decompose(uint64_t total, uint64_t min_slice, uint32_t max_slices, uint64_t* off,
                       uint64_t* len, uint64_t cap);
 
-/* scheduler.cpp:337-364 SchedulerConfig::validate; 0 ok, -1 invalid. */
+/* scheduler.cpp:34-61 SchedulerConfig::validate; 0 ok, -1 invalid. */
 int so_sched_config_validate(const spray_sched_config* c);
 
 typedef struct so_rail {       /* scheduler.hpp:158-168 RailCostState */
@@ -89,11 +89,11 @@ void so_release(so_sched* s, uint32_t rail, uint64_t len);   /* 203-209 */
 void so_feedback(so_sched* s, uint32_t rail, double t_obs_s, double x_norm); /* 208-230 */
 void so_periodic_reset(so_sched* s, uint64_t now);           /* 232-240 */
 void so_reset_rail(so_sched* s, uint32_t rail, uint64_t now);/* 242-247 */
-/* resilience.cpp:162-189 observe (exclusion at 137-148) */
+/* resilience.cpp:71-98 observe (exclusion at 137-148) */
 void so_observe(so_sched* s, uint32_t local, uint32_t remote, int status, double t_obs_s,
                 double predicted_s, uint64_t now);
 
-/* resilience.cpp:191-212, 220-244 */
+/* resilience.cpp:100-121, 220-244 */
 void so_observe_probe(so_sched* s, uint32_t rail, int status, uint64_t now);
 void so_due_probes(so_sched* s, uint64_t now);
 
@@ -129,11 +129,11 @@ int so_state_step(so_state* st, const spray_trace_event* ev, size_t n, spray_dec
 /* LatencyHistogram::bucket_for (telemetry.cpp:10-19) */
 int so_hist_bucket(uint64_t t_ns);
 
-/* sim_backend.cpp:171-181: modelled completion of one slice posted at `now` on a rail
+/* sim_backend.cpp:83-93: modelled completion of one slice posted at `now` on a rail
  * free at `next_free` (no jitter, no faults) */
 uint64_t so_sim_done_ns(uint64_t now, uint64_t next_free, uint64_t len, double bw,
                         double service_factor, double degrade, double latency_us);
-/* sim_backend.cpp:192-200: bytes written by an attempt aborted by a down fault */
+/* sim_backend.cpp:104-112: bytes written by an attempt aborted by a down fault */
 uint64_t so_sim_partial_bytes(uint64_t len, uint64_t start, uint64_t done, uint64_t down_start);
 
 #ifdef __cplusplus

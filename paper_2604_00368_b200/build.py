@@ -44,9 +44,6 @@ def _compile(src: str, flags) -> str:
     path = os.path.join(CSRC, src)
     if _stale(obj, [path] + _headers()):
         cmd = [NVCC] + COMMON + flags + ["-c", path, "-o", obj]
-        if src.endswith(".cpp"):
-            cmd = [NVCC] + COMMON + ["-x", "cu"] + ARCH + flags + ["-c", path, "-o", obj] if False else \
-                  [NVCC] + COMMON + flags + ["-c", path, "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"compile {src} failed:\n{r.stdout}\n{r.stderr}")

@@ -1444,7 +1444,7 @@ void Engine::ce_proxy_loop(int k) {
     return ((f->active >> effect) & 1u) && f->start[effect] <= now && now < f->end[effect];
   };
   auto post = [&](const CeOrder& o, uint32_t status) {
-    // DROP_COMPLETION (sim_backend.cpp:151-156): the bytes landed, the event is lost; the
+    // DROP_COMPLETION (sim_backend.cpp:118-121, 139): the bytes landed, the event is lost; the
     // device's deadline scan times the attempt out
     const uint64_t now = ctl_->device_now;
     if (status == kStOk && (fault_at(o.rail, kFxDrop, now) || fault_at(o.remote, kFxDrop, now))) return;

@@ -165,7 +165,7 @@ Capabilities Capabilities::preset(const std::string& name) {
   Capabilities c;
   c.id = name;
   const uint32_t hh = 1u << 0, hd = 1u << 1, dh = 1u << 3, dd = 1u << 4;
-  if (name == "sim") {  // sim_backend.cpp:96-113
+  if (name == "sim") {  // sim_backend.cpp:9-25
     c.media_mask = hh | hd | dh | dd;
     c.cross_node = true;
     c.same_node = false;

@@ -14,7 +14,7 @@ from oracle.oracle import (EV_BOARD, EV_CHARGE, EV_COMPLETE, EV_DECIDE, EV_DUE_P
                            EV_PROBE_DONE, EV_RELEASE, EV_RESET, EV_RESET_RAIL, EVENT_DTYPE, EVF_CANCELLED,
                            EVF_MODEL, NO_RAIL)
 
-SIM_CAPS = dict(pairs="all", cross=True, same=False)          # sim_backend.cpp:96-113
+SIM_CAPS = dict(pairs="all", cross=True, same=False)          # sim_backend.cpp:9-25
 MEMORY_CAPS = dict(pairs="all", cross=True, same=True)        # memory_backend.cpp:8-19
 
 

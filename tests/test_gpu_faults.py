@@ -1,11 +1,11 @@
 """Timeouts, lost completions, jitter and posting windows on the device (SURVEY.md §8 a12,
 a14, a16).
 
-* DROP_COMPLETION (sim_backend.cpp:151-156): the bytes land but the completion is lost;
+* DROP_COMPLETION (sim_backend.cpp:118-121, 139): the bytes land but the completion is lost;
   the device deadline scan (worker_timeout_phase, engine.cpp:996-1022) times the attempt
   out, handle_failure retries it elsewhere, the batch completes bit-exact
   (test_engine.cpp:236-256; acceptance criterion 9, acceptance.cpp:470-538).
-* JITTER (sim_backend.cpp:48-61): uniform added delay per unit; bytes exact, plans replay.
+* JITTER (sim_backend.cpp:52-63): uniform added delay per unit; bytes exact, plans replay.
 * Posting windows + post-time re-decide (engine.cpp:855-971): a DOWN rail fails at most a
   window of attempts; the slices queued behind it are released and decided again, and the
   RELEASE / DECIDE events replay identically through the oracle and the device replay.

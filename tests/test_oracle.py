@@ -260,7 +260,7 @@ def test_sim_service_kats(co, golden_dir):
 
 
 def test_partial_write_prefix(co):
-    # sim_backend.cpp:192-200: bytes proportional to progress before the down start
+    # sim_backend.cpp:104-112: bytes proportional to progress before the down start
     assert co.lib.so_sim_partial_bytes(1000, 0, 1000, 250) == 250
     assert co.lib.so_sim_partial_bytes(1000, 100, 1100, 50) == 0
 

@@ -339,7 +339,7 @@ def c5(args):
 def congest(args):
     """Injected congestion on C2: the flow sprays over the direct SM rail(s) and any
     --relay-via rails (tier 1); rail --congest-rail is DEGRADEd to --factor of its
-    bandwidth for the whole run (sim_backend.cpp:171-181 semantics on the real fabric).
+    bandwidth for the whole run (sim_backend.cpp:83-93 semantics on the real fabric).
     Telemetry spraying vs the state-blind round-robin policy (a25), same rails."""
     n = args.size
     src, dst = buf(0, n, 61), buf(1, n)
