@@ -49,6 +49,7 @@ def parse():
     p.add_argument("--lat-batches", type=int, default=200, help="small batches timed for the batch-latency percentiles")
     p.add_argument("--lat-intents", type=int, default=64, help="intents per latency batch (half offload, half reload)")
     p.add_argument("--no-congestion", action="store_true")
+    p.add_argument("--no-small", action="store_true", help="skip the small-slice HBM->HBM sub-line")
     p.add_argument("--no-nvlink", action="store_true", help="N>1: skip the NVLink phase (elephant, broadcast chain, fault)")
     p.add_argument("--nvl-bytes", type=int, default=1 << 30, help="N>1: bytes per elephant flow (C2 shape)")
     p.add_argument("--bcast-bytes", type=int, default=16 << 30, help="N>1: broadcast size (C4 shape)")
@@ -123,7 +124,8 @@ def run_reference(args):
         "config": {"workload": f"kv_batch {args.blocks}x{args.block_kib}KiB, reference CPU engine "
                                f"(memory backend, real clock, {threads} rails/workers: the best of 1..nproc), "
                                "host->host"},
-        "cpu_baseline": {"value": round(gbs, 3), "unit": "GB/s", "cores": threads, "kind": "reference",
+        "cpu_baseline": {"value": round(gbs, 3), "unit": "GB/s", "cores": threads, "nproc": os.cpu_count(),
+                         "kind": "reference",
                          "sample": f"{args.steps} batches of {args.blocks}x{args.block_kib} KiB"},
         "e2e": {"value": round(gbs, 3), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -212,6 +214,49 @@ def batch_latency(sp, eng, reqs, n_batches, per_batch):
     return {"intents_per_batch": per_batch, "bytes_per_batch": sum(r.length for r in reqs[:per_batch]),
             "batches": len(lat), "p50_us": round(pct(lat, 0.5), 1), "p90_us": round(pct(lat, 0.9), 1),
             "p99_us": round(pct(lat, 0.99), 1), "mean_us": round(sum(lat) / len(lat), 1)}
+
+
+def batch_latency_c(sp, eng, reqs, per_batch, n_batches=1000):
+    """The same percentiles with the rounds timed in C++ (spray_batch_latency: allocate /
+    submit_transfers / await / free through the C-ABI, as a C++ application calls them)."""
+    eng.batch_latency_ns(reqs, per_batch, 50)  # warm
+    us = [x / 1e3 for x in eng.batch_latency_ns(reqs, per_batch, n_batches).tolist()]
+    return {"intents_per_batch": per_batch, "bytes_per_batch": sum(r.length for r in reqs[:per_batch]),
+            "batches": len(us), "p50_us": round(pct(us, 0.5), 2), "p90_us": round(pct(us, 0.9), 2),
+            "p99_us": round(pct(us, 0.99), 2), "mean_us": round(sum(us) / len(us), 2)}
+
+
+def small_slices(sp, fabrics, dev, hbm, hbm2, nb, blk, perm, hbm_peak_gbs, reps=4):
+    """The scheduler-bound regime: nb x blk HBM -> HBM through a random block table (one
+    slice per intent), 1 and 2 rails, prepared intents, drain-mode launch timed by CUDA
+    events. Roofline: the HBM copy roofline (delivered bytes = half the HBM traffic)."""
+    out = {"workload": f"{nb} x {blk >> 10} KiB HBM->HBM, random block table, one slice per intent",
+           "roofline_gbs": round(hbm_peak_gbs / 2, 1),
+           "roofline_source": "MEASURED_PEAKS.json hbm_gbs / 2 (a copy reads and writes each byte)"}
+    for rails in (1, 2):
+        cfg = {"resilience": {"degradation_ratio": 1e9}, "b200": {"chunk_bytes": 65536}}
+        e = sp.Engine(fabrics.two_node(rails, 1.6e12 / rails, backend="cuda"), json.dumps(cfg), dev)
+        e.start()
+        e.register_segment(sp.SegmentDescriptor("s", sp.Medium.DEVICE, "a", [sp.BufferDesc(0, nb * blk, hbm.data_ptr())]))
+        e.register_segment(sp.SegmentDescriptor("d", sp.Medium.DEVICE, "b", [sp.BufferDesc(0, nb * blk, hbm2.data_ptr())]))
+        prep = e.prepare_transfers([sp.TransferRequest("s", i * blk, "d", int(perm[i]) * blk, blk) for i in range(nb)])
+        ms = []
+        for k in range(reps + 2):
+            b = e.allocate_batch()
+            t = prep.run(b)
+            if e.batch_status(b).state != sp.BatchState.COMPLETE:
+                raise RuntimeError("small-slice batch not complete")
+            e.free_batch(b)
+            if k >= 2:
+                ms.append(t)
+        best = min(ms)
+        gbs = nb * blk / (statistics.mean(ms) * 1e-3) / 1e9
+        out[f"rails_{rails}"] = {"gbs": round(gbs, 2), "best_gbs": round(nb * blk / (best * 1e-3) / 1e9, 2),
+                                 "slices_per_s_M": round(nb / (statistics.mean(ms) * 1e-3) / 1e6, 3),
+                                 "frac": round(gbs / (hbm_peak_gbs / 2), 4)}
+        prep.free()
+        e.stop()
+    return out
 
 
 # ------------------------------------------------------------------ injected congestion
@@ -533,8 +578,9 @@ def run_b200(args):
     hbm = torch.empty(pool_bytes, dtype=torch.uint8, device=f"cuda:{dev}")
     hbm2 = torch.zeros(pool_bytes, dtype=torch.uint8, device=f"cuda:{dev}")
     sp.fill_splitmix(dev, hbm.data_ptr(), pool_bytes, 1000 + rank)
-    host = torch.zeros(pool_bytes, dtype=torch.uint8, pin_memory=True)
-    host2 = torch.empty(pool_bytes, dtype=torch.uint8, pin_memory=True)
+    # the pinned-host staging pools of this GPU's PCIe root, on the root's NUMA node
+    hbuf, hbuf2 = sp.NumaHostBuffer(dev, pool_bytes), sp.NumaHostBuffer(dev, pool_bytes)
+    host, host2 = hbuf.tensor(), hbuf2.tensor()
     host2.copy_(hbm.cpu())
     for sid, med, t in (("kv/hbm", sp.Medium.DEVICE, hbm), ("kv/hbm2", sp.Medium.DEVICE, hbm2),
                         ("kv/host", sp.Medium.HOST, host), ("kv/host2", sp.Medium.HOST, host2)):
@@ -605,6 +651,11 @@ def run_b200(args):
 
     e2e_step_ms = step_t
     lat = batch_latency(sp, eng, reqs, args.lat_batches, args.lat_intents) if args.lat_batches else None
+    lat_c = None
+    if args.lat_batches:
+        one = [sp.TransferRequest("kv/hbm", int(p_off[i]) * blk, "kv/host", i * blk, 4096) for i in range(256)]
+        lat_c = {"intent_4k_hbm_to_host": batch_latency_c(sp, eng, one, 1),
+                 "kv_batch": batch_latency_c(sp, eng, reqs, args.lat_intents)}
 
     # ---- state-blind baseline: round-robin cudaMemcpyAsync striping of the same blocks
     # (one call per block from C++, the same interleaved order, 4 streams)
@@ -629,6 +680,17 @@ def run_b200(args):
     total_ms, e2e_ms, rr_ms = vals.tolist()
     eng.stop()
 
+    small = None
+    if rank == 0 and not args.no_small:
+        try:
+            peak = 6544.7
+            try:
+                peak = float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"])
+            except Exception:
+                pass
+            small = small_slices(sp, fabrics, dev, hbm, hbm2, nb, blk, p_off, peak)
+        except Exception as ex:  # reported, never fatal
+            small = {"error": str(ex)[:300]}
     cong = None
     if rank == 0 and not args.no_congestion:
         try:
@@ -676,7 +738,10 @@ def run_b200(args):
                                    f"{args.block_kib} KiB reload pinned host->HBM per GPU, random block tables, "
                                    f"one batch of {2 * nb} intents per step, offloads and reloads alternating in "
                                    f"runs of {args.group}",
-                       "fabric": f"{args.sm_rails} SM PCIe rail(s) + {args.ce_rails} copy-engine rail(s) per GPU (kv_offload)", "bytes_per_step_per_gpu": step_bytes,
+                       "fabric": f"{args.sm_rails} SM PCIe rail(s) + {args.ce_rails} copy-engine rail(s) per GPU (kv_offload)",
+                       "bytes_per_step_per_gpu": step_bytes,
+                       "host_pools": f"pinned + device-mapped, NUMA node {hbuf.node} of GPU {dev}'s PCIe root "
+                                     f"(spray_host_alloc_numa; -1 = host reports no node, first-touch placement)",
                        "l2": "inputs (2 x 256 MiB pools) larger than the 126 MB L2",
                        "parallelism": f"weak x{world} (one batch per GPU, no data-path collective)"},
             "e2e": {"value": round(e2e, 3), "unit": "GB/s",
@@ -695,11 +760,14 @@ def run_b200(args):
                                                         "p90_ms": round(pct(e2e_step_ms, 0.9), 3),
                                                         "steps": len(e2e_step_ms)},
                               "small_batches": lat,
+                              "small_batches_cpp": lat_c,
                               "how": "submit -> batch terminal through the public C-ABI, one batch in flight; "
                                      "exact_percentile as bench.cpp:213-215"},
             "gpu_launches": 2 * args.steps,
             "clocks": clk.summary(),
         }
+        if small is not None:
+            line["small_slices"] = small
         if cong is not None:
             line["congestion"] = cong
         if nvl is not None:
@@ -710,7 +778,7 @@ def run_b200(args):
                 if r:
                     gbs, iters, cores = r
                     line["cpu_baseline"] = {"value": round(gbs, 3), "unit": "GB/s", "cores": cores,
-                                            "kind": "reference",
+                                            "nproc": os.cpu_count(), "kind": "reference",
                                             "sample": f"best of {iters} batches of {nb} x {args.block_kib} KiB "
                                                       "host->host through the reference Engine (memory backend, "
                                                       "real clock, 2 rails / 2 workers)"}

@@ -151,6 +151,12 @@ int spray_submit_transfers(spray_engine* e, uint64_t batch, const spray_transfer
 int spray_batch_status(spray_engine* e, uint64_t batch, spray_batch_status_t* out);
 int spray_await_batch(spray_engine* e, uint64_t batch, uint64_t limit_ns, spray_batch_status_t* out);
 int spray_free_batch(spray_engine* e, uint64_t batch);
+/* Batch latency through the calls above, as a C++ caller sees it (bench.cpp:156-157,
+ * 213-215: submit -> batch terminal): n_batches rounds of allocate / submit_transfers
+ * (per_batch requests, cycling through reqs) / await / free, one batch in flight;
+ * lat_ns[i] = the round's steady-clock nanoseconds. Measurement helper, not data path. */
+int spray_batch_latency(spray_engine* e, const spray_transfer_request* reqs, size_t n_reqs, size_t per_batch,
+                        size_t n_batches, uint64_t* lat_ns);
 
 /* Introspection. */
 int spray_rail_count(spray_engine* e, uint32_t* n);
@@ -447,6 +453,13 @@ int spray_checksum(int device, const void* ptr, uint64_t n, uint64_t* out);
 /* Pinned, device-mapped host allocation (cudaHostAlloc Portable|Mapped). */
 int spray_host_alloc(uint64_t n, void** out);
 int spray_host_free(void* p);
+/* NUMA node of a GPU's PCIe root (-1 when the host reports none). */
+int spray_device_numa_node(int device, int32_t* node);
+/* Pinned, device-mapped host memory placed on `device`'s NUMA node (mbind + first touch,
+ * then cudaHostRegister Mapped|Portable): the pinned-host staging pool of one PCIe root.
+ * *node_out = the node the pages are bound to (-1: not bound, first-touch placement). */
+int spray_host_alloc_numa(int device, uint64_t n, void** out, int32_t* node_out);
+int spray_host_free_numa(void* p);
 
 /* State-blind striping baseline (the Policy::kRoundRobin analog a25,
  * scheduler.cpp:175-177): copy n (src[i], dst[i], len[i]) ranges with one

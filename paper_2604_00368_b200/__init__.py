@@ -9,7 +9,8 @@ from .engine import (BatchState, BatchStatus, BufferDesc, CapabilityError, Compl
                      InvalidRangeError, Medium, NoRouteError, PostResult, Prepared, RailStats, Requests,
                      SegmentDescriptor,
                      SliceWorkRequest, StagedRoute, TransferRequest, checksum, fill_splitmix, hash128, host_alloc, host_free, rr_copy,
-                     IPC_HANDLE_BYTES, board_bytes, ipc_close, ipc_export, ipc_open)
+                     IPC_HANDLE_BYTES, NumaHostBuffer, board_bytes, device_numa_node, ipc_close, ipc_export,
+                     ipc_open)
 from . import fabrics  # noqa: F401
 
 __all__ = ["Engine", "CudaBackend", "TransferRequest", "SegmentDescriptor", "BufferDesc", "Direction", "Medium",

@@ -103,6 +103,7 @@ _SIGS = {
     "spray_batch_status": (C.c_int, [P, C.c_uint64, C.POINTER(BatchStatusC)]),
     "spray_await_batch": (C.c_int, [P, C.c_uint64, C.c_uint64, C.POINTER(BatchStatusC)]),
     "spray_free_batch": (C.c_int, [P, C.c_uint64]),
+    "spray_batch_latency": (C.c_int, [P, C.POINTER(TransferRequestC), C.c_size_t, C.c_size_t, C.c_size_t, U64P]),
     "spray_rail_count": (C.c_int, [P, C.POINTER(C.c_uint32)]),
     "spray_rail_id": (C.c_int, [P, C.c_uint32, C.c_char_p, C.c_size_t]),
     "spray_rail_stats_get": (C.c_int, [P, C.c_uint32, C.POINTER(RailStatsC)]),
@@ -133,6 +134,9 @@ _SIGS = {
     "spray_checksum": (C.c_int, [C.c_int, P, C.c_uint64, U64P]),
     "spray_host_alloc": (C.c_int, [C.c_uint64, VP]),
     "spray_host_free": (C.c_int, [P]),
+    "spray_device_numa_node": (C.c_int, [C.c_int, C.POINTER(C.c_int32)]),
+    "spray_host_alloc_numa": (C.c_int, [C.c_int, C.c_uint64, VP, C.POINTER(C.c_int32)]),
+    "spray_host_free_numa": (C.c_int, [P]),
     "spray_rr_copy": (C.c_int, [C.c_int, U64P, U64P, U64P, C.c_size_t, C.c_int, C.POINTER(C.c_double)]),
     "spray_ipc_export": (C.c_int, [C.c_int, P, P]),
     "spray_ipc_open": (C.c_int, [C.c_int, P, VP]),

@@ -2,6 +2,9 @@
 // cross it: each entry maps the reference exception class to its SPRAY_E* code and
 // keeps the message in a thread-local buffer (spray_last_error).
 #include <cuda_runtime.h>
+#include <sys/mman.h>
+#include <sys/syscall.h>
+#include <unistd.h>
 
 #include <algorithm>
 #include <chrono>
@@ -128,6 +131,29 @@ int spray_await_batch(spray_engine* e, uint64_t batch, uint64_t limit_ns, spray_
   return guard([&] { *out = e->eng->await_batch(batch, limit_ns); });
 }
 int spray_free_batch(spray_engine* e, uint64_t batch) { return guard([&] { e->eng->free_batch(batch); }); }
+
+// Batch latency as a C++ application sees it (bench.cpp:156-157, 213-215: submit -> batch
+// terminal): n_batches rounds of allocate_batch, submit_transfers(per_batch requests, cycling
+// through reqs), await_batch, free_batch, one batch in flight, through the same public calls
+// as above. lat_ns[i] = steady-clock nanoseconds of round i.
+int spray_batch_latency(spray_engine* e, const spray_transfer_request* reqs, size_t n_reqs, size_t per_batch,
+                        size_t n_batches, uint64_t* lat_ns) {
+  return guard([&] {
+    if (per_batch == 0 || per_batch > n_reqs) throw ConfigError("batch_latency: per_batch must be in [1, n_reqs]");
+    const size_t groups = n_reqs / per_batch;
+    for (size_t i = 0; i < n_batches; ++i) {
+      const spray_transfer_request* g = reqs + (i % groups) * per_batch;
+      const auto t0 = std::chrono::steady_clock::now();
+      const uint64_t b = e->eng->allocate_batch();
+      e->eng->submit_transfers(b, g, per_batch, nullptr);
+      const spray_batch_status_t st = e->eng->await_batch(b, 60'000'000'000ull);
+      if (st.state != SPRAY_BATCH_COMPLETE) throw EngineError("batch_latency: batch did not complete");
+      e->eng->free_batch(b);
+      lat_ns[i] = static_cast<uint64_t>(
+          std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now() - t0).count());
+    }
+  });
+}
 
 int spray_rail_count(spray_engine* e, uint32_t* n) { return guard([&] { *n = e->eng->rail_count(); }); }
 int spray_rail_id(spray_engine* e, uint32_t rail, char* buf, size_t cap) {
@@ -342,7 +368,7 @@ int spray_replay_device(int device, const spray_sched_config* sc, const spray_re
       auto* out = static_cast<unsigned long long*>(dev(2 * sizeof(unsigned long long)));
       auto* fin = static_cast<RailState*>(dev(sizeof(RailState) * n_rails));
       CK(spray_launch::launch_replay(E, ev, n_events, dd, dcap, out, fin, 0));
-      CK(cudaDeviceSynchronize());
+      CK(cudaStreamSynchronize(0));
       unsigned long long o[2];
       CK(cudaMemcpy(o, out, sizeof(o), cudaMemcpyDeviceToHost));
       *n_dec = o[0];
@@ -361,7 +387,7 @@ int spray_fill_splitmix(int device, void* ptr, uint64_t n, uint64_t seed) {
   return guard([&] {
     CK(cudaSetDevice(device));
     CK(spray_launch::launch_fill(ptr, n, seed, 0));
-    CK(cudaDeviceSynchronize());
+    CK(cudaStreamSynchronize(0));  // not the device: a persistent engine kernel may be resident
   });
 }
 
@@ -373,7 +399,7 @@ int spray_checksum(int device, const void* ptr, uint64_t n, uint64_t* out) {
     cudaMemset(d, 0, sizeof(unsigned long long));
     cudaError_t e = spray_launch::launch_checksum(ptr, n, d, 0);
     unsigned long long v = 0;
-    if (e == cudaSuccess) e = cudaDeviceSynchronize();
+    if (e == cudaSuccess) e = cudaStreamSynchronize(0);
     if (e == cudaSuccess) e = cudaMemcpy(&v, d, sizeof(v), cudaMemcpyDeviceToHost);
     cudaFree(d);
     CK(e);
@@ -385,6 +411,79 @@ int spray_host_alloc(uint64_t n, void** out) {
   return guard([&] { CK(cudaHostAlloc(out, n, cudaHostAllocMapped | cudaHostAllocPortable)); });
 }
 int spray_host_free(void* p) { return guard([&] { CK(cudaFreeHost(p)); }); }
+
+// NUMA node of a GPU's PCIe root: /sys/bus/pci/devices/<bus id>/numa_node (-1: unknown or
+// a single-node host).
+static int numa_node_of(int device) {
+  char bus[32] = {0};
+  if (cudaDeviceGetPCIBusId(bus, sizeof(bus), device) != cudaSuccess) {
+    cudaGetLastError();
+    return -1;
+  }
+  std::string id(bus);
+  for (char& c : id) c = static_cast<char>(std::tolower(static_cast<unsigned char>(c)));
+  std::FILE* f = std::fopen(("/sys/bus/pci/devices/" + id + "/numa_node").c_str(), "r");
+  if (!f) return -1;
+  int node = -1;
+  if (std::fscanf(f, "%d", &node) != 1) node = -1;
+  std::fclose(f);
+  return node;
+}
+
+static std::mutex g_numa_mu;
+static std::map<void*, size_t> g_numa_allocs;
+
+int spray_device_numa_node(int device, int32_t* node) {
+  return guard([&] { *node = numa_node_of(device); });
+}
+
+// Pinned host memory on the GPU's own NUMA node: anonymous pages bound there with mbind
+// (MPOL_BIND, strict) and faulted in before cudaHostRegister pins and maps them, so the
+// PCIe root's DMA and the SM copies never cross the socket interconnect. Falls back to
+// first-touch placement when the node is unknown.
+int spray_host_alloc_numa(int device, uint64_t n, void** out, int32_t* node_out) {
+  return guard([&] {
+    if (n == 0) throw ConfigError("host_alloc_numa: zero bytes");
+    const size_t len = (n + (2u << 20) - 1) & ~size_t((2u << 20) - 1);
+    void* p = mmap(nullptr, len, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS, -1, 0);
+    if (p == MAP_FAILED) throw EngineError("host_alloc_numa: mmap failed");
+    const int node = numa_node_of(device);
+    int bound = -1;
+    if (node >= 0 && node < 1024) {
+      unsigned long mask[1024 / (8 * sizeof(unsigned long))] = {0};
+      mask[node / (8 * sizeof(unsigned long))] |= 1ul << (node % (8 * sizeof(unsigned long)));
+      constexpr int kMpolBind = 2, kMfStrict = 1, kMfMove = 2;
+      if (syscall(SYS_mbind, p, len, kMpolBind, mask, 1024ul, kMfStrict | kMfMove) == 0) bound = node;
+    }
+    std::memset(p, 0, len);  // fault every page in on the bound node
+    const cudaError_t e = cudaHostRegister(p, len, cudaHostRegisterMapped | cudaHostRegisterPortable);
+    if (e != cudaSuccess) {
+      munmap(p, len);
+      CK(e);
+    }
+    {
+      std::lock_guard<std::mutex> lk(g_numa_mu);
+      g_numa_allocs[p] = len;
+    }
+    *out = p;
+    if (node_out) *node_out = bound;
+  });
+}
+
+int spray_host_free_numa(void* p) {
+  return guard([&] {
+    size_t len = 0;
+    {
+      std::lock_guard<std::mutex> lk(g_numa_mu);
+      auto it = g_numa_allocs.find(p);
+      if (it == g_numa_allocs.end()) throw EngineError("host_free_numa: not a spray_host_alloc_numa pointer");
+      len = it->second;
+      g_numa_allocs.erase(it);
+    }
+    CK(cudaHostUnregister(p));
+    munmap(p, len);
+  });
+}
 
 int spray_rr_copy(int device, const uint64_t* src, const uint64_t* dst, const uint64_t* len, size_t n, int streams,
                   double* ms_out) {

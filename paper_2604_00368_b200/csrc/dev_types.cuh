@@ -51,7 +51,8 @@ struct RailState {
   int32_t backoff;
   int32_t probe_streak;
   uint32_t probe_inflight;
-  uint32_t pad_;
+  uint32_t beta_epoch;     // bumped whenever beta0/beta1/min_obs change other than by adopting
+                           // the FEEDBACK warp's chain result (its stale-result check)
   uint64_t next_probe, excluded_at;
   uint64_t bytes_posted, bytes_ok, bytes_failed;
   uint32_t hist[48];
@@ -220,6 +221,8 @@ struct alignas(64) Control {
   // 2 first decision, 3 last decision, 4 first completion applied, 5 last completion
   // applied, 6 scheduler exit
   volatile uint64_t tl[8];
+  volatile uint64_t dbg[16];         // diagnostic words (relay 0: hop-1 / hop-2 tickets, slots 0-3's
+                                     // free rounds and descriptor stamps, exit generation)
 };
 
 // Telemetry window cell (telemetry.hpp:37-44 WindowCell), one per rail per window in an

@@ -15,6 +15,7 @@ cudaError_t launch_engine(const spray_dev::EngineDev& E, int grid, int block, cu
 cudaError_t launch_epoch(uint64_t* out, cudaStream_t st);
 cudaError_t launch_relay_forward(const spray_dev::EngineDev& E, uint32_t r, int grid, cudaStream_t st);
 cudaError_t launch_hold(const uint32_t* flag, cudaStream_t st);
+cudaError_t preload_kernels();
 }  // namespace spray_launch
 
 namespace spray {
@@ -251,6 +252,7 @@ Engine::~Engine() {
 
 void Engine::alloc_device() {
   CK(cudaSetDevice(device_));
+  CK(spray_launch::preload_kernels());  // no lazy load may wait behind the persistent kernel
   CK(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
   CK(cudaStreamCreateWithFlags(&copy_stream_, cudaStreamNonBlocking));
   auto host = [&](size_t bytes) -> void* {
@@ -480,6 +482,7 @@ void Engine::setup_relay(uint32_t idx, int via) {
     int ok = 0;
     if (j != via && cudaDeviceCanAccessPeer(&ok, via, j) == cudaSuccess && ok) enable(j);
   }
+  CK(spray_launch::preload_kernels());  // the forwarder launches on `via` while engines run
   RelayHost h;
   h.via = via;
   CK(cudaStreamCreateWithFlags(&h.stream, cudaStreamNonBlocking));
@@ -1356,6 +1359,9 @@ void Engine::debug_words(uint64_t* out, size_t n) {
     v.push_back(static_cast<uint64_t>(ctl_->xc_tail));
     v.push_back(static_cast<uint64_t>(ctl_->xc_head));
     for (int q = 0; q < 8; ++q) v.push_back(static_cast<uint64_t>(ctl_->tl[q]));  // words 37..44
+    // words 45..60: device diagnostic words (Control::dbg), 61: this launch's generation
+    for (int q = 0; q < 16; ++q) v.push_back(static_cast<uint64_t>(ctl_->dbg[q]));
+    v.push_back(E_.launch_gen);
   }
   for (size_t i = 0; i < n; ++i) out[i] = i < v.size() ? v[i] : 0;
 }

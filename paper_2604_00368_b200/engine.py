@@ -258,6 +258,15 @@ class Engine:
         _check(lib.spray_free_batch(self._h, batch))
 
     # ---- device-resident submission
+    def batch_latency_ns(self, reqs, per_batch: int, n_batches: int) -> np.ndarray:
+        """Per-batch submit -> terminal latency (ns) of n_batches rounds of allocate / submit
+        (per_batch requests) / await / free, timed in C++ (spray_batch_latency)."""
+        r = reqs if isinstance(reqs, Requests) else Requests(reqs)
+        out = np.zeros(n_batches, dtype=np.uint64)
+        _check(lib.spray_batch_latency(self._h, r.arr, len(r), per_batch, n_batches,
+                                       out.ctypes.data_as(C.POINTER(C.c_uint64))))
+        return out
+
     def prepare_transfers(self, reqs: Sequence[TransferRequest]) -> "Prepared":
         arr, keep = _reqs_c(reqs)
         p = C.c_void_p()
@@ -538,6 +547,37 @@ def host_alloc(n: int) -> int:
 
 def host_free(p: int):
     _check(lib.spray_host_free(p))
+
+
+def device_numa_node(device: int) -> int:
+    """NUMA node of the GPU's PCIe root (-1 when unknown)."""
+    n = C.c_int32()
+    _check(lib.spray_device_numa_node(device, C.byref(n)))
+    return n.value
+
+
+class NumaHostBuffer:
+    """Pinned, device-mapped host memory on the GPU's own NUMA node (spray_host_alloc_numa):
+    the pinned-host staging pool of one PCIe root. `.ptr`, `.node`, and a zero-copy uint8
+    `torch` / `numpy` view of the first n bytes."""
+
+    def __init__(self, device: int, n: int):
+        p = C.c_void_p()
+        node = C.c_int32()
+        _check(lib.spray_host_alloc_numa(device, n, C.byref(p), C.byref(node)))
+        self.ptr, self.n, self.node = p.value, n, node.value
+
+    def numpy(self):
+        return np.ctypeslib.as_array((C.c_uint8 * self.n).from_address(self.ptr))
+
+    def tensor(self):
+        import torch
+        return torch.from_numpy(self.numpy())
+
+    def free(self):
+        if self.ptr:
+            _check(lib.spray_host_free_numa(self.ptr))
+            self.ptr = 0
 
 
 def board_bytes(n_slots: int) -> int:

@@ -1,0 +1,56 @@
+// lat_bench.cu — dependent-chain latency (cycles per op) of the primitives on the STATE
+// warp's serial decision path: FP64 mul/add, IEEE FP64 division, uniform-datapath warp
+// reduction (REDUX), double shuffle, 32-bit modulo, ballot+popc.
+#include <cstdio>
+#include <cstdint>
+#define N 4096
+__global__ void k(double* out, long long* cyc, double a0, uint32_t m0) {
+  const int lane = threadIdx.x & 31;
+  double a = a0 + lane * 1e-9, b = 1.0000001;
+  uint32_t u = m0 + lane;
+  long long t0, t1;
+  // DMUL chain
+  t0 = clock64();
+  for (int i = 0; i < N; ++i) a = __dmul_rn(a, b);
+  t1 = clock64(); if (lane == 0) cyc[0] = t1 - t0;
+  // DADD chain
+  t0 = clock64();
+  for (int i = 0; i < N; ++i) a = __dadd_rn(a, 1e-12);
+  t1 = clock64(); if (lane == 0) cyc[1] = t1 - t0;
+  // division chain
+  t0 = clock64();
+  for (int i = 0; i < N / 8; ++i) a = __ddiv_rn(a + 1.0, 1.0000003);
+  t1 = clock64(); if (lane == 0) cyc[2] = (t1 - t0) * 8;
+  // REDUX min chain
+  t0 = clock64();
+  for (int i = 0; i < N; ++i) u = __reduce_min_sync(0xffffffffu, u + (uint32_t)lane) + 1u;
+  t1 = clock64(); if (lane == 0) cyc[3] = t1 - t0;
+  // double shuffle chain
+  t0 = clock64();
+  for (int i = 0; i < N; ++i) a = __shfl_xor_sync(0xffffffffu, a, 1) + 1e-12;
+  t1 = clock64(); if (lane == 0) cyc[4] = t1 - t0;
+  // 32-bit modulo chain
+  t0 = clock64();
+  for (int i = 0; i < N; ++i) u = (u * 2654435761u + 7u) % (3u + (u & 7u));
+  t1 = clock64(); if (lane == 0) cyc[5] = t1 - t0;
+  // ballot + popc chain
+  t0 = clock64();
+  for (int i = 0; i < N; ++i) u = __popc(__ballot_sync(0xffffffffu, ((u + lane) & 1u) != 0)) + u;
+  t1 = clock64(); if (lane == 0) cyc[6] = t1 - t0;
+  // DSETP + select chain (min of doubles)
+  t0 = clock64();
+  for (int i = 0; i < N; ++i) a = (a < b) ? a + 1e-9 : b - 1e-9;
+  t1 = clock64(); if (lane == 0) cyc[7] = t1 - t0;
+  out[lane] = a + u;
+}
+int main() {
+  double* o; long long* c; cudaMalloc(&o, 256); cudaMalloc(&c, 64);
+  k<<<1, 32>>>(o, c, 1.0, 3); cudaDeviceSynchronize();
+  k<<<1, 32>>>(o, c, 1.0, 3);
+  long long h[8]; cudaMemcpy(h, c, 64, cudaMemcpyDeviceToHost);
+  const char* names[8] = {"dmul", "dadd", "ddiv_rn", "redux_min", "shfl_xor_f64", "mod_u32", "ballot_popc", "dsetp_sel"};
+  printf("{");
+  for (int i = 0; i < 8; ++i) printf("%s\"%s\": %.1f", i ? ", " : "", names[i], (double)h[i] / N);
+  printf("}\n");
+  return 0;
+}

@@ -15,7 +15,7 @@ from paper_2604_00368_b200 import _lib as L, fabrics  # noqa: E402
 
 NAMES = ["host_tail", "sub_tail", "sub_head", "state", "now", "disp", "term", "failed", "retried", "trace_n",
          "stream", "loops", "serial", "obs", "fb", "n_comp", "n_dec", "apply", "decide", "ctl", "ingress", "complete",
-         "egress", "egress_blocks", "ingress_blocks", "entries", "pub_busy", "rx_busy", "n_fences", "p1", "p2", "p3",
+         "egress", "egress_blocks", "ingress_blocks", "entries", "pub_busy", "rx_busy", "n_fences", "p1", "p2", "fb_busy",
          "scans"]
 
 
@@ -50,7 +50,7 @@ for rails in (1, 2, 4):
         best = min(ms[2:])
         gbs = nb * blk / (best * 1e-3) / 1e9
         ghz = 1.9e9
-        keys = ("apply", "decide", "ctl", "serial", "obs", "fb", "complete", "egress", "ingress", "pub_busy", "p1", "p2", "p3")
+        keys = ("apply", "decide", "ctl", "serial", "obs", "fb", "complete", "egress", "ingress", "pub_busy", "p1", "p2", "fb_busy")
         row = {"rails": rails, "chunk": chunk, "gbs": round(gbs, 1), "ms": round(best, 4),
                "slices_per_s_M": round(nb / (best * 1e-3) / 1e6, 2), "entries": d["entries"], "loops": d["loops"]}
         row.update({kk + "_ms": round(d[kk] / ghz * 1e3, 3) for kk in keys})
