@@ -221,6 +221,9 @@ struct alignas(64) Control {
   // 2 first decision, 3 last decision, 4 first completion applied, 5 last completion
   // applied, 6 scheduler exit
   volatile uint64_t tl[8];
+  volatile uint64_t lat[8];          // b200.diag: engine ns of the last pass of each pipeline stage
+                                     // (HOSTRX fetch, INGRESS block, STATE decide, EGRESS post,
+                                     // PUBLISH stamp, COMPLETE gather, STATE apply, PUBLISH done)
   volatile uint64_t dbg[16];         // diagnostic words (relay 0: hop-1 / hop-2 tickets, slots 0-3's
                                      // free rounds and descriptor stamps, exit generation)
 };
@@ -277,14 +280,29 @@ struct RelayDesc {  // 32 B, in K's HBM: written by the hop-1 worker, read by th
   uint32_t len, slice, target, gen;  // target = units of the attempt, gen = its generation
   uint64_t stamp;   // (launch_gen << 32) | (ticket + 1), release-stored last
 };
+// Host-staged relay (the staged route, engine.cpp:465-610: D2H into a bounded pinned-host
+// pool, H2D out of it, pipelined; needs no peer access): staging, descriptors, slot rounds,
+// the exit generation and a ticket-indexed completion ring live in mapped pinned host
+// memory. The forwarder on K cannot touch this engine's counters, so it posts each forwarded
+// chunk into `done[ticket % n_slots]` (stamped last); HOSTRX drains that ring in ticket order
+// into COMPLETE, like copy-engine completions, and publishes `consumed` (this GPU's HBM),
+// which hop 1 checks before reusing a ring position.
+struct RelayDone {
+  uint32_t slice, gen, target, pad_;  // target: units | drop flag (bit 31)
+  uint64_t stamp;                     // (launch_gen << 32) | (ticket + 1), release-stored last
+  uint64_t pad2_;
+};
 struct RelayDev {
-  uint8_t* staging;             // K's HBM: n_slots x chunk_bytes
-  RelayDesc* desc;              // K's HBM: n_slots descriptors
-  uint32_t* exit_gen;           // K's HBM: the engine writes its launch generation on exit
-  uint32_t* seq;                // this GPU's HBM: per-slot free round (forwarder -> workers)
+  uint8_t* staging;             // K's HBM (host-staged: pinned host): n_slots x chunk_bytes
+  RelayDesc* desc;              // K's HBM (host-staged: pinned host): n_slots descriptors
+  uint32_t* exit_gen;           // K's HBM (host-staged: pinned host): launch generation on exit
+  uint32_t* seq;                // this GPU's HBM (host-staged: pinned host): per-slot free round
   unsigned long long* tail;     // this GPU's HBM: hop-1 ticket counter (workers)
   unsigned long long* head;     // K's HBM: hop-2 ticket counter (forwarder warps)
+  RelayDone* done;              // host-staged only: pinned host completion ring
+  unsigned long long* consumed; // host-staged only: this GPU's HBM, done records HOSTRX drained
   uint32_t n_slots, via;        // power of two; relay GPU ordinal
+  uint32_t host_staged, pad_;
 };
 
 // GlobalLoadBoard slot (scheduler.hpp:66-90) in caller-owned shared host memory: one per
@@ -344,9 +362,10 @@ struct EngineDev {
   double degradation_ratio, degradation_min_t;
   uint32_t max_attempts;
   uint32_t has_ce;                             // poll the CE proxy completion ring
+  uint32_t has_staged;                         // host-staged relays: poll their done rings
   uint64_t slice_timeout_ns;                   // ResilienceConfig::slice_timeout (0 = none)
   uint32_t fence_batch;                        // chunks a copy warp moves per system fence (1..4)
-  uint32_t pad_fb_;
+  uint32_t diag;                               // write the per-stage timeline words (Control::lat)
   uint64_t timeout_scan_ns;                    // deadline scan period of the TIMER warp
   uint64_t probe_interval, probe_bytes;        // resilience.hpp:23-26
   double probe_backoff_mult;

@@ -8,6 +8,8 @@
 #include <deque>
 #include <cstring>
 #include <immintrin.h>
+#include <set>
+#include <tuple>
 
 namespace spray_launch {
 size_t engine_smem_bytes();
@@ -176,10 +178,15 @@ EngineOptions engine_options_from_json(const std::string& text) {
     if (j.contains("b200")) {
       const Json& b = j.at("b200");
       reject_unknown(b, {"grid", "block", "chunk_bytes", "idle_exit_ms", "slice_capacity", "work_capacity",
-                         "sub_capacity", "batch_slots", "gate_timeout_ms", "post_window", "fence_batch"},
+                         "sub_capacity", "batch_slots", "gate_timeout_ms", "post_window", "fence_batch", "diag",
+                         "no_peer", "staged_routes"},
                      "b200");
       eo.post_window = static_cast<uint32_t>(b.number_or("post_window", eo.post_window));
       eo.fence_batch = static_cast<uint32_t>(b.number_or("fence_batch", eo.fence_batch));
+      if (b.contains("diag")) eo.diag = b.at("diag").as_bool();
+      if (b.contains("staged_routes")) eo.staged_routes = b.at("staged_routes").as_bool();
+      if (b.contains("no_peer"))
+        for (const Json& g : b.at("no_peer").arr) eo.no_peer.push_back(static_cast<int>(g.as_number()));
       if (eo.fence_batch < 1 || eo.fence_batch > 4) throw ConfigError("b200.fence_batch must be in [1, 4]");
       if (b.contains("gate_timeout_ms"))
         eo.gate_timeout_ns = static_cast<uint64_t>(b.at("gate_timeout_ms").as_number() * 1e6);
@@ -209,6 +216,7 @@ Engine::Engine(EngineOptions opts, const std::string& topology_json, int device)
     : opts_(std::move(opts)), topo_(Topology::parse(topology_json)), device_(device) {
   validate(opts_.sched, opts_.diffusion_weight);
   validate(opts_.res);
+  synthesize_staged_routes();
   if (opts_.backends.empty()) throw ConfigError("engine: no backends configured");
   for (const std::string& b : opts_.backends) caps_.push_back(Capabilities::preset(b));
   if (topo_.rail_count() > size_t(kMaxRails)) throw ConfigError("topology: more than 64 rails per engine");
@@ -240,6 +248,62 @@ Engine::Engine(EngineOptions opts, const std::string& topology_json, int device)
   }
   host_only_sm_ = n_dev_nodes == 1 && n_sm > 0 && n_sm_host == n_sm;
   slot_busy_.assign(opts_.batch_slots, 0);
+}
+
+// Staged-route synthesis (orchestrator.cpp:120-234, engine.cpp:465-610): a GPU node this
+// engine's GPU has no peer access to (cudaDeviceCanAccessPeer, or b200.no_peer) cannot be
+// reached by direct rails. With b200.staged_routes (default on) the engine declares a
+// host-staged relay rail pair towards it (<own node>.st<K>, <K's node>.st<K>): hop 1 stores
+// into a bounded pinned-host pool, a forwarder on GPU K drains it into K's HBM. Planning
+// then routes transfers into K over that rail only (set_for), and keeps it out of every
+// route a direct rail can serve.
+void Engine::synthesize_staged_routes() {
+  std::string own;
+  for (const NodeDecl& nd : topo_.nodes())
+    if (topo_.node_gpu(nd.id) == device_) own = nd.id;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess) {
+    cudaGetLastError();
+    ndev = 0;
+  }
+  std::vector<std::pair<std::string, int>> far;
+  for (const NodeDecl& nd : topo_.nodes()) {
+    const int g = topo_.node_gpu(nd.id);
+    if (g < 0 || g == device_) continue;
+    bool peer = true;
+    if (std::find(opts_.no_peer.begin(), opts_.no_peer.end(), g) != opts_.no_peer.end()) {
+      peer = false;
+    } else if (g < ndev && device_ < ndev) {
+      int ok = 1;
+      if (cudaDeviceCanAccessPeer(&ok, device_, g) != cudaSuccess) cudaGetLastError(), ok = 1;
+      peer = ok != 0;
+    }
+    if (!peer) {
+      no_peer_gpus_.insert(g);
+      far.emplace_back(nd.id, g);
+    }
+  }
+  if (!opts_.staged_routes || own.empty()) return;
+  for (const auto& [node, g] : far) {
+    const std::string tag = ".st" + std::to_string(g);
+    if (topo_.rail_index(own + tag)) continue;  // declared by the application
+    RailDecl a;
+    a.id = own + tag;
+    a.node = own;
+    a.backend = "cuda";
+    a.bandwidth = 55e9;  // a pinned-host pool: one PCIe Gen5 x16 crossing each way
+    a.tier = 1;
+    a.executor = 2;
+    a.gpu = device_;
+    a.via = g < ndev ? g : device_;  // (test boxes with fewer GPUs: the forwarder runs here)
+    a.host_staged = true;
+    topo_.add_rail(a);
+    RailDecl b = a;
+    b.id = node + tag;
+    b.node = node;
+    b.gpu = g;
+    if (!topo_.rail_index(b.id)) topo_.add_rail(b);
+  }
 }
 
 Engine::~Engine() {
@@ -301,7 +365,7 @@ void Engine::alloc_device() {
   std::vector<RailDesc> rd(nr);
   std::vector<RailState> rs(nr);
   const auto ranks = topo_.id_ranks();
-  std::vector<std::pair<uint32_t, int>> relay_rails;  // (relay index, via GPU)
+  std::vector<std::tuple<uint32_t, int, bool>> relay_rails;  // (relay index, via GPU, host staged)
   for (uint32_t i = 0; i < nr; ++i) {
     const RailDecl& r = topo_.rail(i);
     rd[i] = RailDesc{};
@@ -311,7 +375,8 @@ void Engine::alloc_device() {
     // ring can then never overrun the proxy)
     {
       const uint32_t warps = static_cast<uint32_t>(std::max(1, launch_grid() - 1)) * (opts_.block / 32);
-      const uint32_t w = opts_.post_window ? opts_.post_window : (r.executor == 1 ? 2048u : std::max(64u, 2 * warps));
+      uint32_t w = opts_.post_window ? opts_.post_window : (r.executor == 1 ? 2048u : std::max(64u, 2 * warps));
+      if (r.host_staged && !opts_.post_window) w = 2048;  // the staging pool's slots
       rd[i].window = r.executor == 1 ? std::min<uint32_t>(w, ce_cap / 2) : w;
     }
     rd[i].bandwidth = r.bandwidth;
@@ -324,7 +389,7 @@ void Engine::alloc_device() {
     if (r.executor == 2) {
       if (relay_rails.size() >= size_t(kMaxRelays)) throw ConfigError("more than 8 relay rails");
       rd[i].ce_index = static_cast<uint32_t>(relay_rails.size());
-      relay_rails.emplace_back(rd[i].ce_index, r.via);
+      relay_rails.emplace_back(rd[i].ce_index, r.via, r.host_staged);
     }
     // probe counterparts (resilience.cpp:17-44): same-backend rails on other nodes, the
     // 1:1 affinity partner first, nodes in id order; node-local backends probe themselves
@@ -380,6 +445,7 @@ void Engine::alloc_device() {
   E_.pend_pos = static_cast<uint64_t*>(dev(sizeof(uint64_t) * 2 * kMaxRails));
   E_.slice_timeout_ns = opts_.res.slice_timeout_ns;
   E_.fence_batch = opts_.fence_batch;
+  E_.diag = opts_.diag ? 1u : 0u;
   // the deadline scan runs ~8 times per timeout (the reference's wheel has 10 ms buckets,
   // engine.cpp:18), bounded to [0.2, 10] ms
   E_.timeout_scan_ns = std::min<uint64_t>(10'000'000, std::max<uint64_t>(200'000, opts_.res.slice_timeout_ns / 8));
@@ -447,8 +513,10 @@ void Engine::alloc_device() {
   CK(cudaStreamSynchronize(copy_stream_));
   ctl_->epoch = E_.epoch;
   ctl_->idle_exit_ns = opts_.idle_exit_ns;
-  for (const auto& rr : relay_rails) setup_relay(rr.first, rr.second);
+  for (const auto& rr : relay_rails) setup_relay(std::get<0>(rr), std::get<1>(rr), std::get<2>(rr));
   E_.n_relays = static_cast<uint32_t>(relay_rails.size());
+  E_.has_staged = 0;
+  for (const auto& rr : relay_rails) E_.has_staged |= std::get<2>(rr) ? 1u : 0u;
   if (has_ce_) {
     ce_streams_.resize(8);
     for (auto& s : ce_streams_) CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
@@ -459,37 +527,41 @@ void Engine::alloc_device() {
 // GPU's HBM (hop 2 reads them locally), the slot-free rounds and the ticket counter here
 // (hop 1 polls them locally). Peer access: this GPU <-> via both ways (staging stores,
 // completion atomics), via -> every other GPU it can reach (hop-2 destinations).
-void Engine::setup_relay(uint32_t idx, int via) {
+void Engine::setup_relay(uint32_t idx, int via, bool host_staged) {
   int n = 0;
   CK(cudaGetDeviceCount(&n));
   if (via >= n) throw ConfigError("relay rail: via GPU " + std::to_string(via) + " does not exist");
-  int a = 1, b = 1;
-  if (via != device_) {
-    CK(cudaDeviceCanAccessPeer(&a, device_, via));
-    CK(cudaDeviceCanAccessPeer(&b, via, device_));
-  }
-  if (!a || !b) throw ConfigError("relay rail: no peer access between GPU " + std::to_string(device_) + " and " +
-                                  std::to_string(via));
   auto enable = [](int peer) {
     const cudaError_t e = cudaDeviceEnablePeerAccess(peer, 0);
     if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) CK(e);
     cudaGetLastError();
   };
-  CK(cudaSetDevice(device_));
-  if (via != device_) enable(via);
-  CK(cudaSetDevice(via));
-  for (int j = 0; j < n; ++j) {
-    int ok = 0;
-    if (j != via && cudaDeviceCanAccessPeer(&ok, via, j) == cudaSuccess && ok) enable(j);
+  if (!host_staged) {  // device staging: hop 1 stores into K's HBM, hop 2 counts in ours
+    int a = 1, b = 1;
+    if (via != device_) {
+      CK(cudaDeviceCanAccessPeer(&a, device_, via));
+      CK(cudaDeviceCanAccessPeer(&b, via, device_));
+    }
+    if (!a || !b) throw ConfigError("relay rail: no peer access between GPU " + std::to_string(device_) + " and " +
+                                    std::to_string(via) + " (declare it \"staging\": \"host\")");
+    CK(cudaSetDevice(device_));
+    if (via != device_) enable(via);
+    CK(cudaSetDevice(via));
+    for (int j = 0; j < n; ++j) {
+      int ok = 0;
+      if (j != via && cudaDeviceCanAccessPeer(&ok, via, j) == cudaSuccess && ok) enable(j);
+    }
   }
+  CK(cudaSetDevice(via));
   CK(spray_launch::preload_kernels());  // the forwarder launches on `via` while engines run
   RelayHost h;
   h.via = via;
   CK(cudaStreamCreateWithFlags(&h.stream, cudaStreamNonBlocking));
-  constexpr uint32_t kSlots = 2048;  // power of two
+  constexpr uint32_t kSlots = 2048;  // power of two: 64 MiB of 32 KiB granules (engine.hpp:56-58's pool)
   RelayDev R{};
   R.n_slots = kSlots;
   R.via = static_cast<uint32_t>(via);
+  R.host_staged = host_staged ? 1u : 0u;
   auto on_via = [&](size_t bytes) -> void* {
     void* p = nullptr;
     CK(cudaMalloc(&p, bytes));
@@ -497,17 +569,40 @@ void Engine::setup_relay(uint32_t idx, int via) {
     h.via_allocs.push_back(p);
     return p;
   };
-  R.staging = static_cast<uint8_t*>(on_via(size_t(kSlots) << E_.chunk_shift));
-  R.desc = static_cast<RelayDesc*>(on_via(sizeof(RelayDesc) * kSlots));
-  R.exit_gen = static_cast<uint32_t*>(on_via(sizeof(uint32_t)));
+  auto pinned = [&](size_t bytes) -> void* {  // mapped pinned host memory both GPUs address
+    void* p = nullptr;
+    CK(cudaHostAlloc(&p, bytes, cudaHostAllocMapped | cudaHostAllocPortable));
+    std::memset(p, 0, bytes);
+    h.host_allocs.push_back(p);
+    void* d = nullptr;
+    CK(cudaHostGetDevicePointer(&d, p, 0));
+    return d;
+  };
   R.head = static_cast<unsigned long long*>(on_via(sizeof(unsigned long long)));
+  if (host_staged) {
+    R.staging = static_cast<uint8_t*>(pinned(size_t(kSlots) << E_.chunk_shift));
+    R.desc = static_cast<RelayDesc*>(pinned(sizeof(RelayDesc) * kSlots));
+    R.exit_gen = static_cast<uint32_t*>(pinned(sizeof(uint32_t)));
+    R.seq = static_cast<uint32_t*>(pinned(sizeof(uint32_t) * kSlots));
+    R.done = static_cast<RelayDone*>(pinned(sizeof(RelayDone) * kSlots));
+  } else {
+    R.staging = static_cast<uint8_t*>(on_via(size_t(kSlots) << E_.chunk_shift));
+    R.desc = static_cast<RelayDesc*>(on_via(sizeof(RelayDesc) * kSlots));
+    R.exit_gen = static_cast<uint32_t*>(on_via(sizeof(uint32_t)));
+  }
   CK(cudaSetDevice(device_));
-  R.seq = static_cast<uint32_t*>(nullptr);
   void* p = nullptr;
-  CK(cudaMalloc(&p, sizeof(uint32_t) * kSlots));
-  CK(cudaMemset(p, 0, sizeof(uint32_t) * kSlots));
-  dev_allocs_.push_back(p);
-  R.seq = static_cast<uint32_t*>(p);
+  if (!host_staged) {
+    CK(cudaMalloc(&p, sizeof(uint32_t) * kSlots));
+    CK(cudaMemset(p, 0, sizeof(uint32_t) * kSlots));
+    dev_allocs_.push_back(p);
+    R.seq = static_cast<uint32_t*>(p);
+  } else {
+    CK(cudaMalloc(&p, sizeof(unsigned long long)));
+    CK(cudaMemset(p, 0, sizeof(unsigned long long)));
+    dev_allocs_.push_back(p);
+    R.consumed = static_cast<unsigned long long*>(p);
+  }
   CK(cudaMalloc(&p, sizeof(unsigned long long)));
   CK(cudaMemset(p, 0, sizeof(unsigned long long)));
   dev_allocs_.push_back(p);
@@ -529,6 +624,7 @@ void Engine::free_device() {
     cudaSetDevice(h.via);
     if (h.stream) cudaStreamSynchronize(h.stream), cudaStreamDestroy(h.stream);
     for (void* p : h.via_allocs) cudaFree(p);
+    for (void* p : h.host_allocs) cudaFreeHost(p);
   }
   relays_.clear();
   cudaSetDevice(device_);
@@ -752,7 +848,8 @@ uint32_t Engine::set_for(const Segment& src, const Segment& dst, Direction dir) 
   if (it != set_cache_.end()) return it->second;
   CK(cudaSetDevice(device_));
   auto routes = build_plan(topo_, src, dst, dir, opts_.sched.penalty, caps_);  // throws NoRouteError
-  const Route& r = routes.front();
+  Route r = routes.front();
+  filter_staged(r, src, dst);
   if (r.candidates.size() > size_t(kMaxLocals)) throw ConfigError("route has more than 32 local rails");
   if (sets_.size() >= opts_.max_sets) throw EngineError("candidate-set table full");
   CandSet cs{};
@@ -785,10 +882,33 @@ std::vector<int32_t> Engine::plan_candidates(const std::string& s, const std::st
   if (si == segs_.end() || di == segs_.end()) throw EngineError("unknown segment id");
   auto routes = build_plan(topo_, si->second.seg, di->second.seg, dir == SPRAY_READ ? Direction::kRead : Direction::kWrite,
                            opts_.sched.penalty, caps_);
-  if (backend) *backend = routes.front().backend;
+  Route r = routes.front();
+  filter_staged(r, si->second.seg, di->second.seg);
+  if (backend) *backend = r.backend;
   std::vector<int32_t> out{1};
-  append_stream(out, routes.front().candidates);
+  append_stream(out, r.candidates);
   return out;
+}
+
+// Staged routes only where no direct route exists (orchestrator.cpp:120-122): into a GPU
+// without peer access, keep just the host-staged relay rails; everywhere else, drop them.
+// A staged route starts at this engine's GPU: moving out of a GPU without peer access
+// needs an engine there.
+void Engine::filter_staged(Route& r, const Segment& src, const Segment& dst) const {
+  auto far = [&](const Segment& s) {
+    return s.medium == Medium::kDevice && no_peer_gpus_.count(topo_.node_gpu(s.node)) != 0;
+  };
+  if (far(src))
+    throw NoRouteError("NoRoute: '" + src.id + "' is on a GPU without peer access; staged routes start at GPU " +
+                       std::to_string(device_));
+  const bool staged = far(dst);
+  std::vector<LocalCandidate> keep;
+  for (const LocalCandidate& c : r.candidates)
+    if (topo_.rail(c.local).host_staged == staged) keep.push_back(c);
+  if (keep.empty())
+    throw NoRouteError(staged ? "NoRoute: no staged route into '" + dst.id + "' (b200.staged_routes off)"
+                              : "NoRoute: no direct rail connects '" + src.id + "' -> '" + dst.id + "'");
+  r.candidates = std::move(keep);
 }
 
 uint64_t Engine::decompose_count(uint64_t len) const {  // scheduler.cpp:94-106
@@ -1285,8 +1405,12 @@ void Engine::rail_stats(uint32_t rail, spray_rail_stats* out) {
   if (rail >= rail_count()) throw EngineError("bad rail index");
   std::memset(out, 0, sizeof(*out));
   if (!rmirror_) return;
+  // the scheduler writes its rail states to HBM whenever it goes quiet (and at exit), so a
+  // caller that saw a batch complete reads stats that include its completions
   RailState s;
-  std::memcpy(&s, const_cast<const RailState*>(&rmirror_[rail]), sizeof(s));
+  CK(cudaSetDevice(device_));
+  CK(cudaMemcpyAsync(&s, &E_.rail_state[rail], sizeof(s), cudaMemcpyDeviceToHost, copy_stream_));
+  CK(cudaStreamSynchronize(copy_stream_));
   out->bytes_posted = s.bytes_posted;
   out->bytes_ok = s.bytes_ok;
   out->bytes_failed = s.bytes_failed;
@@ -1362,6 +1486,7 @@ void Engine::debug_words(uint64_t* out, size_t n) {
     // words 45..60: device diagnostic words (Control::dbg), 61: this launch's generation
     for (int q = 0; q < 16; ++q) v.push_back(static_cast<uint64_t>(ctl_->dbg[q]));
     v.push_back(E_.launch_gen);
+    for (int q = 0; q < 8; ++q) v.push_back(static_cast<uint64_t>(ctl_->lat[q]));  // words 62..69
   }
   for (size_t i = 0; i < n; ++i) out[i] = i < v.size() ? v[i] : 0;
 }

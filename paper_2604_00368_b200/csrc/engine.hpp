@@ -11,6 +11,7 @@
 #include <atomic>
 #include <cstdint>
 #include <map>
+#include <set>
 #include <mutex>
 #include <string>
 #include <thread>
@@ -44,6 +45,9 @@ struct EngineOptions {
   uint64_t window_ns = 10'000'000;              // telemetry window (stats_window_ms)
   uint32_t fence_batch = 4;                      // chunks a copy warp copies per system fence when
                                                  // its next chunk is already queued (1 = every chunk)
+  bool diag = false;                             // per-stage timeline words (Control::lat)
+  bool staged_routes = true;                     // synthesize host-staged routes to GPUs without peer access
+  std::vector<int> no_peer;                      // GPUs treated as lacking peer access (testing / policy)
   uint32_t post_window = 0;                      // units in flight per rail (0: 2 x worker warps for
                                                  // SM/relay rails, 2048 orders for CE rails)
 };
@@ -155,6 +159,9 @@ class Engine {
   uint64_t allocate_batch_locked();
   void free_batch_locked(uint64_t batch);
   uint64_t decompose_count(uint64_t len) const;
+  void synthesize_staged_routes();
+  void filter_staged(Route& r, const Segment& src, const Segment& dst) const;
+  std::set<int> no_peer_gpus_;
 
   EngineOptions opts_;
   Topology topo_;
@@ -197,13 +204,14 @@ class Engine {
     int via = -1;
     cudaStream_t stream = nullptr;    // on the relay GPU
     std::vector<void*> via_allocs;    // staging, descriptors, exit generation
+    std::vector<void*> host_allocs;   // host-staged relays: the pinned pool and its rings
   };
   std::vector<RelayHost> relays_;
   void* board_registered_ = nullptr;  // host board this engine registered (unregistered on free)
   volatile uint32_t* hold_ = nullptr;  // mapped flag of the timed-run stream hold
   uint32_t* hold_dev_ = nullptr;
   uint32_t launch_gen_ = 0;
-  void setup_relay(uint32_t idx, int via);
+  void setup_relay(uint32_t idx, int via, bool host_staged);
   void sync_relays();
   bool host_only_sm_ = false;  // every SM rail stages through pinned host memory
   static constexpr int kHostLinkCtas = 48;

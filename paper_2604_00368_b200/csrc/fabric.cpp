@@ -66,6 +66,10 @@ Topology Topology::parse(const std::string& text) {
       r.gpu = static_cast<int>(jr.number_or("gpu", -1));
       r.via = static_cast<int>(jr.number_or("via", -1));
       r.ce_index = static_cast<uint32_t>(jr.number_or("ce_index", 0));
+      const std::string stg = jr.string_or("staging", "device");
+      if (stg != "device" && stg != "host") throw ConfigError("rail '" + r.id + "': staging must be device or host");
+      r.host_staged = stg == "host";
+      if (r.host_staged && r.executor != 2) throw ConfigError("rail '" + r.id + "': host staging is for relay rails");
       t.rails_.push_back(std::move(r));
     }
   } catch (const JsonError& e) {
@@ -143,6 +147,27 @@ const DeviceDecl* Topology::first_device_of_kind(const std::string& node_id, Dev
   for (const DeviceDecl& d : n->devices)
     if (d.kind == kind) return &d;
   return nullptr;
+}
+
+RailIndex Topology::add_rail(const RailDecl& r) {
+  if (!node(r.node)) throw ConfigError("rail '" + r.id + "': dangling node reference '" + r.node + "'");
+  const RailIndex i = static_cast<RailIndex>(rails_.size());
+  if (!by_id_.emplace(r.id, i).second) throw ConfigError("duplicate rail id '" + r.id + "'");
+  rails_.push_back(r);
+  auto& v = by_node_backend_[{r.node, r.backend}];
+  v.push_back(i);
+  std::sort(v.begin(), v.end(), [&](RailIndex a, RailIndex b) { return rails_[a].id < rails_[b].id; });
+  for (const DeviceDecl& d : node(r.node)->devices) {
+    auto it = links_.find(d.id);
+    if (it != links_.end()) it->second[i] = r.tier;
+  }
+  return i;
+}
+
+int Topology::node_gpu(const std::string& n) const {
+  for (const RailDecl& r : rails_)
+    if (r.node == n && r.gpu >= 0) return r.gpu;
+  return -1;
 }
 
 std::vector<uint32_t> Topology::id_ranks() const {

@@ -65,6 +65,8 @@ struct RailDecl {
   uint32_t executor = 0;   // 0 sm, 1 ce, 2 relay
   int gpu = -1, via = -1;
   uint32_t ce_index = 0;
+  bool host_staged = false;  // relay through a bounded pinned-host pool ("staging": "host"):
+                             // the staged route of engine.cpp:465-610, no peer access needed
 };
 
 class Topology {
@@ -84,6 +86,11 @@ class Topology {
   const DeviceDecl* first_device_of_kind(const std::string& node, DeviceKind kind) const;
   // Rank of each rail's id string in sorted order (string-order tie-breaks on device).
   std::vector<uint32_t> id_ranks() const;
+  // Appends a rail (staged-route synthesis): linked at tier `tier` to every device of its
+  // node that has explicit links, indices rebuilt.
+  RailIndex add_rail(const RailDecl& r);
+  // GPU ordinal a node's rails declare ("gpu" key), -1 if none.
+  int node_gpu(const std::string& node) const;
 
  private:
   std::vector<NodeDecl> nodes_;

@@ -23,10 +23,15 @@ def _node(g: int, host: bool = True) -> Dict:
 
 
 def kv_offload(gpu: int = 0, sm_rails: int = 1, ce_rails: int = 0, bw_sm: float = PCIE5_X16,
-               bw_ce: float = PCIE5_X16) -> str:
+               bw_ce: float = PCIE5_X16, relay_via: Optional[List[int]] = None, bw_relay: float = PCIE5_X16) -> str:
     """HiCache-style KV offload on one GPU (config 3): HBM <-> pinned host over the GPU's
-    PCIe root. Host memory links only to the PCIe rails; HBM links to all."""
+    PCIe root. Host memory links only to the PCIe rails; HBM links to all. `relay_via` adds
+    one 2-hop rail per listed GPU K (g.rlK): hop 1 over NVLink into K's HBM, hop 2 by K's
+    SMs over K's own PCIe root, so the host staging spans several roots."""
     rails, links = [], []
+    for v in relay_via or []:
+        rails.append({"id": f"g{gpu}.rl{v}", "node": f"g{gpu}", "bandwidth_bytes_per_sec": bw_relay,
+                      "affinity": "direct", "backend": "cuda", "executor": "relay", "via": v, "gpu": gpu})
     for i in range(sm_rails):
         rails.append({"id": f"g{gpu}.pcie{i}", "node": f"g{gpu}", "bandwidth_bytes_per_sec": bw_sm,
                       "affinity": "direct", "backend": "cuda", "executor": "sm"})

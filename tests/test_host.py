@@ -163,3 +163,48 @@ def test_relay_rail_without_via_is_a_config_error():
         r.pop("via", None)
     with pytest.raises(sp.ConfigError):
         sp.Engine(json.dumps(topo), json.dumps({}))
+
+
+def _locals(e, s):
+    locs, k = [], 2
+    for _ in range(s[1]):
+        locs.append(e.rail_id(s[k]))
+        k += 2 + 3 * s[k + 1]
+    return locs
+
+
+def test_staged_route_synthesized_for_gpu_without_peer_access():
+    """Staged-route synthesis (orchestrator.cpp:120-234): with GPU 1 lacking peer access
+    (b200.no_peer), the engine on GPU 0 declares a host-staged relay rail pair towards it
+    and routes g0 -> g1 over that rail alone; a host destination keeps the direct rails
+    (staged only where no direct route exists); a transfer starting on GPU 1 has no route
+    from this engine."""
+    topo = fabrics.peer_fabric([0, 1], sm_rails=1)
+    e = sp.Engine(topo, json.dumps({"b200": {"no_peer": [1]}}), 0)
+    ids = [e.rail_id(r) for r in range(e.rail_count())]
+    assert "g0.st1" in ids and "g1.st1" in ids
+    e.register_segment(sp.SegmentDescriptor("s", sp.Medium.DEVICE, "g0", [sp.BufferDesc(0, 1 << 20, 0x1000)]))
+    e.register_segment(sp.SegmentDescriptor("d", sp.Medium.DEVICE, "g1", [sp.BufferDesc(0, 1 << 20, 0x2000)]))
+    e.register_segment(sp.SegmentDescriptor("h", sp.Medium.HOST, "g0", [sp.BufferDesc(0, 1 << 20, 0x3000)]))
+    s, _ = e.plan_candidates("s", "d")
+    assert _locals(e, s) == ["g0.st1"]
+    s, _ = e.plan_candidates("s", "h")
+    assert "g0.st1" not in _locals(e, s) and "g0.nvl0" in _locals(e, s)
+    with pytest.raises(sp.NoRouteError):
+        e.plan_candidates("d", "s")
+
+
+def test_staged_routes_off_leaves_no_route():
+    topo = fabrics.peer_fabric([0, 1], sm_rails=1)
+    e = sp.Engine(topo, json.dumps({"b200": {"no_peer": [1], "staged_routes": False}}), 0)
+    e.register_segment(sp.SegmentDescriptor("s", sp.Medium.DEVICE, "g0", [sp.BufferDesc(0, 1 << 20, 0x1000)]))
+    e.register_segment(sp.SegmentDescriptor("d", sp.Medium.DEVICE, "g1", [sp.BufferDesc(0, 1 << 20, 0x2000)]))
+    with pytest.raises(sp.NoRouteError):
+        e.plan_candidates("s", "d")
+
+
+def test_host_staging_is_for_relay_rails():
+    topo = json.loads(fabrics.peer_fabric([0, 1], sm_rails=1))
+    topo["rails"][0]["staging"] = "host"
+    with pytest.raises(sp.ConfigError):
+        sp.Engine(json.dumps(topo), json.dumps({}))

@@ -1,0 +1,43 @@
+"""Where a single 4 KiB intent's latency goes: the engine runs with b200.diag, each round is
+one batch (allocate / submit / await / free, timed in C++), and after each round the
+per-stage timeline words (Control::lat, engine ns of each stage's last pass) are read.
+Reported as stage-to-stage deltas (median over rounds)."""
+import ctypes as C
+import json
+import os
+import sys
+import time
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2604_00368_b200 as sp  # noqa: E402
+from paper_2604_00368_b200 import _lib as L, fabrics  # noqa: E402
+
+STAGES = ["hostrx_fetch", "ingress_block", "state_decide", "egress_post", "publish_stamp", "complete_gather",
+          "state_apply", "publish_done"]
+n = 1 << 20
+e = sp.Engine(fabrics.two_node(1, 1e9, backend="cuda"),
+              json.dumps({"resilience": {"degradation_ratio": 1e9}, "b200": {"diag": True}}), 0)
+e.start()
+src = torch.empty(n, dtype=torch.uint8, device="cuda:0")
+dst = torch.zeros(n, dtype=torch.uint8, device="cuda:0")
+e.register_segment(sp.SegmentDescriptor("s", sp.Medium.DEVICE, "a", [sp.BufferDesc(0, n, src.data_ptr())]))
+e.register_segment(sp.SegmentDescriptor("d", sp.Medium.DEVICE, "b", [sp.BufferDesc(0, n, dst.data_ptr())]))
+reqs = [sp.TransferRequest("s", 4096 * i, "d", 4096 * i, 4096) for i in range(64)]
+e.batch_latency_ns(reqs, 1, 50)
+deltas, tot = [], []
+w = (C.c_uint64 * 72)()
+for k in range(200):
+    t = e.batch_latency_ns(reqs, 1, 1)[0]
+    L.lib.spray_engine_debug(e._h, w, 72)
+    lat = list(w)[62:70]
+    deltas.append([lat[i + 1] - lat[i] for i in range(7)])
+    tot.append(t)
+d = np.median(np.array(deltas, dtype=np.int64), axis=0)
+out = {"round_us_median": round(float(np.median(tot)) / 1e3, 2),
+       "device_span_us": round(float(np.median([sum(x) for x in deltas])) / 1e3, 2),
+       "stage_deltas_us": {f"{STAGES[i]}->{STAGES[i + 1]}": round(float(d[i]) / 1e3, 2) for i in range(7)}}
+print(json.dumps(out, indent=1), flush=True)
+os._exit(0)

@@ -34,7 +34,7 @@ st = e.await_batch(b, 10_000_000_000)
 w = (C.c_uint64 * 64)()
 L.lib.spray_engine_debug(e._h, w, 64)
 print("state", st, "debug", list(w), flush=True)
-print("relay tail/head/seq0/stamp0/exit_gen", list(w)[45:50], "out_slices/fb_head/cq_head", list(w)[50:53],
+print("relay tail/head/seq0/stamp0/exit_gen", list(w)[45:50], 
       "seq[0:4]", list(w)[53:57], "stamp[0:4]", [hex(x) for x in list(w)[57:61]], "launch_gen", w[61], flush=True)
 print("bytes ok", [(e.rail_id(r), e.rail_stats(r).bytes_ok) for r in range(e.rail_count())], flush=True)
 if st.state == sp.BatchState.COMPLETE:
