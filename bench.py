@@ -266,7 +266,9 @@ def congestion(sp, fabrics, dev, hbm, host, nb, blk, perm, reps=4):
     (sim_backend.cpp:83-93 semantics on the real fabric: FIFO service at factor x B)
     throttles g.pcie1 to 10% for the whole run. Workload: the offload half of the KV batch.
     The cost model only (degradation exclusion off), so the difference is the scheduler's."""
-    out = {"workload": f"{nb} x {blk >> 10} KiB offload HBM->pinned host per batch",
+    out = {"kind": "software throttle: a DEGRADE fault (FIFO service at 10% of B on g.pcie1) inside the "
+                   "engine's own copy workers, not real contention (see congestion_real at N > 1)",
+           "workload": f"{nb} x {blk >> 10} KiB offload HBM->pinned host per batch",
            "fabric": "2 SM rails on one PCIe root, g.pcie1 DEGRADE factor 0.1",
            "exclusion": "off (degradation_ratio 1e9): cost-model steering only"}
     for pol in ("telemetry", "round_robin"):
@@ -571,6 +573,7 @@ def run_b200(args):
     pool_bytes = blk * nb
 
     cfg = {"resilience": {"degradation_ratio": 1e9}, "b200": {"chunk_bytes": 65536}}
+    cfg["b200"].update(json.loads(os.environ.get("SPRAY_BENCH_B200", "{}")))  # experiments: engine knobs
     eng = sp.Engine(fabrics.kv_offload(dev, sm_rails=args.sm_rails, ce_rails=args.ce_rails, bw_ce=args.ce_gbs * 1e9),
                     json.dumps(cfg), dev)
     eng.start()

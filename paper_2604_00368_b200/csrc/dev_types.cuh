@@ -351,6 +351,8 @@ struct EngineDev {
   uint8_t* trace_ev; uint8_t* trace_dec; uint64_t trace_cap;  // HBM (spray_trace_event / spray_decision)
   uint64_t* persist;                           // HBM: scheduler scalars persisted across launches
   FaultDev* faults_hbm;                        // HBM mirror of the fault words (workers read)
+  uint32_t* faults_any;                        // HBM: 1 while any fault word is active (HOSTRX)
+  uint32_t* any_failed;                        // HBM: 1 once any batch failed (COMPLETE's cancel check)
   unsigned long long* next_free;               // HBM degrade FIFO server per rail
   uint32_t* exit_flag;                         // HBM: scheduler -> workers
 

@@ -450,6 +450,8 @@ void Engine::alloc_device() {
   // engine.cpp:18), bounded to [0.2, 10] ms
   E_.timeout_scan_ns = std::min<uint64_t>(10'000'000, std::max<uint64_t>(200'000, opts_.res.slice_timeout_ns / 8));
   E_.faults_hbm = static_cast<FaultDev*>(dev(sizeof(FaultDev) * kMaxRails));
+  E_.faults_any = static_cast<uint32_t*>(dev(sizeof(uint32_t)));
+  E_.any_failed = static_cast<uint32_t*>(dev(sizeof(uint32_t)));
   E_.next_free = static_cast<unsigned long long*>(dev(sizeof(unsigned long long) * kMaxRails));
   {  // telemetry windows: every cell starts empty (window = ~0)
     const size_t tb = sizeof(TeleCell) * kTeleWindows * std::max<size_t>(1, topo_.rail_count());
