@@ -368,6 +368,8 @@ struct EngineDev {
   uint64_t slice_timeout_ns;                   // ResilienceConfig::slice_timeout (0 = none)
   uint32_t fence_batch;                        // chunks a copy warp moves per system fence (1..4)
   uint32_t diag;                               // write the per-stage timeline words (Control::lat)
+  uint32_t worker_fence_sys;                   // copy warps fence at system scope (else GPU scope)
+  uint32_t pad_wf_;
   uint64_t timeout_scan_ns;                    // deadline scan period of the TIMER warp
   uint64_t probe_interval, probe_bytes;        // resilience.hpp:23-26
   double probe_backoff_mult;

@@ -179,11 +179,16 @@ EngineOptions engine_options_from_json(const std::string& text) {
       const Json& b = j.at("b200");
       reject_unknown(b, {"grid", "block", "chunk_bytes", "idle_exit_ms", "slice_capacity", "work_capacity",
                          "sub_capacity", "batch_slots", "gate_timeout_ms", "post_window", "fence_batch", "diag",
-                         "no_peer", "staged_routes"},
+                         "no_peer", "staged_routes", "worker_fence"},
                      "b200");
       eo.post_window = static_cast<uint32_t>(b.number_or("post_window", eo.post_window));
       eo.fence_batch = static_cast<uint32_t>(b.number_or("fence_batch", eo.fence_batch));
       if (b.contains("diag")) eo.diag = b.at("diag").as_bool();
+      if (b.contains("worker_fence")) {
+        const std::string wf = b.at("worker_fence").as_string();
+        if (wf != "sys" && wf != "gpu") throw ConfigError("b200.worker_fence must be sys or gpu");
+        eo.worker_fence_sys = wf == "sys";
+      }
       if (b.contains("staged_routes")) eo.staged_routes = b.at("staged_routes").as_bool();
       if (b.contains("no_peer"))
         for (const Json& g : b.at("no_peer").arr) eo.no_peer.push_back(static_cast<int>(g.as_number()));
@@ -370,12 +375,15 @@ void Engine::alloc_device() {
     const RailDecl& r = topo_.rail(i);
     rd[i] = RailDesc{};
     // posting window (SimBackend inflight_window, sim_backend.cpp:81): units in flight per
-    // rail. SM / relay rails: twice the worker warps, so one rail alone keeps every copy warp
-    // busy with a second chunk queued; CE rails: orders, at most half the proxy ring (the
+    // rail. SM / relay rails: a copy warp holds up to fence_batch counted-late chunks plus its
+    // prefetched ticket, so twice (fence_batch + 1) chunks per warp keep one rail alone
+    // saturating every warp with work queued (tools/gpu/run_c3.sh: 2 x warps throttles the
+    // KV batch by 7% at fence_batch 4); CE rails: orders, at most half the proxy ring (the
     // ring can then never overrun the proxy)
     {
       const uint32_t warps = static_cast<uint32_t>(std::max(1, launch_grid() - 1)) * (opts_.block / 32);
-      uint32_t w = opts_.post_window ? opts_.post_window : (r.executor == 1 ? 2048u : std::max(64u, 2 * warps));
+      uint32_t w = opts_.post_window ? opts_.post_window
+                                     : (r.executor == 1 ? 2048u : std::max(64u, 2 * (opts_.fence_batch + 1) * warps));
       if (r.host_staged && !opts_.post_window) w = 2048;  // the staging pool's slots
       rd[i].window = r.executor == 1 ? std::min<uint32_t>(w, ce_cap / 2) : w;
     }
@@ -446,6 +454,7 @@ void Engine::alloc_device() {
   E_.slice_timeout_ns = opts_.res.slice_timeout_ns;
   E_.fence_batch = opts_.fence_batch;
   E_.diag = opts_.diag ? 1u : 0u;
+  E_.worker_fence_sys = opts_.worker_fence_sys ? 1u : 0u;
   // the deadline scan runs ~8 times per timeout (the reference's wheel has 10 ms buckets,
   // engine.cpp:18), bounded to [0.2, 10] ms
   E_.timeout_scan_ns = std::min<uint64_t>(10'000'000, std::max<uint64_t>(200'000, opts_.res.slice_timeout_ns / 8));

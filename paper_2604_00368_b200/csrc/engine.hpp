@@ -43,9 +43,10 @@ struct EngineOptions {
   uint32_t max_sets = 1024;
   uint64_t gate_timeout_ns = 10'000'000'000ull;  // dataflow gate wait before an attempt fails
   uint64_t window_ns = 10'000'000;              // telemetry window (stats_window_ms)
-  uint32_t fence_batch = 4;                      // chunks a copy warp copies per system fence when
+  uint32_t fence_batch = 2;                      // chunks a copy warp copies per system fence when
                                                  // its next chunk is already queued (1 = every chunk)
   bool diag = false;                             // per-stage timeline words (Control::lat)
+  bool worker_fence_sys = true;                  // copy warps' fence scope before counting a chunk
   bool staged_routes = true;                     // synthesize host-staged routes to GPUs without peer access
   std::vector<int> no_peer;                      // GPUs treated as lacking peer access (testing / policy)
   uint32_t post_window = 0;                      // units in flight per rail (0: 2 x worker warps for

@@ -43,10 +43,50 @@ __global__ void k(double* out, long long* cyc, double a0, uint32_t m0) {
   t1 = clock64(); if (lane == 0) cyc[7] = t1 - t0;
   out[lane] = a + u;
 }
+
+// __nanosleep granularity and global-memory round trips (one warp, lane 0)
+__global__ void k2(unsigned long long* g, long long* cyc) {
+  if (threadIdx.x != 0) return;
+  long long t0, t1;
+  const int n = 256;
+  for (int s = 0; s < 4; ++s) {
+    const unsigned ns = 32u << (2 * s);  // 32, 128, 512, 2048
+    t0 = clock64();
+    for (int i = 0; i < n; ++i) __nanosleep(ns);
+    t1 = clock64();
+    cyc[8 + s] = (t1 - t0) / n;
+  }
+  // dependent L2 loads (ld.acquire.gpu), atomics, CAS
+  unsigned long long v = 0;
+  t0 = clock64();
+  for (int i = 0; i < n; ++i) {
+    unsigned int x;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(x) : "l"(g + (v & 1)) : "memory");
+    v += x + 1;
+  }
+  t1 = clock64(); cyc[12] = (t1 - t0) / n;
+  t0 = clock64();
+  for (int i = 0; i < n; ++i) v += atomicAdd(g + 2 + (v & 1), 1ull);
+  t1 = clock64(); cyc[13] = (t1 - t0) / n;
+  t0 = clock64();
+  for (int i = 0; i < n; ++i) v += atomicCAS(g + 4, v, v + 1);
+  t1 = clock64(); cyc[14] = (t1 - t0) / n;
+  t0 = clock64();
+  for (int i = 0; i < n; ++i) { __threadfence_system(); v += clock64() & 1; }
+  t1 = clock64(); cyc[15] = (t1 - t0) / n;
+  g[6] = v;
+}
 int main() {
-  double* o; long long* c; cudaMalloc(&o, 256); cudaMalloc(&c, 64);
+  double* o; long long* c; cudaMalloc(&o, 256); cudaMalloc(&c, 16 * 8);
   k<<<1, 32>>>(o, c, 1.0, 3); cudaDeviceSynchronize();
   k<<<1, 32>>>(o, c, 1.0, 3);
+  unsigned long long* g; cudaMalloc(&g, 64); cudaMemset(g, 0, 64);
+  long long* c2; cudaMalloc(&c2, 16 * 8);
+  k2<<<1, 32>>>(g, c2); cudaDeviceSynchronize();
+  long long h2[16]; cudaMemcpy(h2, c2, 16 * 8, cudaMemcpyDeviceToHost);
+  printf("{\"nanosleep_32\": %lld, \"nanosleep_128\": %lld, \"nanosleep_512\": %lld, \"nanosleep_2048\": %lld, "
+         "\"ld_acquire_gpu\": %lld, \"atomic_add\": %lld, \"atomic_cas\": %lld, \"fence_sys_idle\": %lld}\n",
+         h2[8], h2[9], h2[10], h2[11], h2[12], h2[13], h2[14], h2[15]);
   long long h[8]; cudaMemcpy(h, c, 64, cudaMemcpyDeviceToHost);
   const char* names[8] = {"dmul", "dadd", "ddiv_rn", "redux_min", "shfl_xor_f64", "mod_u32", "ballot_popc", "dsetp_sel"};
   printf("{");

@@ -24,13 +24,15 @@ ap.add_argument("--blocks", type=int, default=4096)
 args = ap.parse_args()
 
 blk, nb = 64 << 10, args.blocks
-e = sp.Engine(fabrics.kv_offload(0), json.dumps({"resilience": {"degradation_ratio": 1e9}, "b200": {"chunk_bytes": 65536}}), 0)
+b200 = {"chunk_bytes": 65536}
+b200.update(json.loads(os.environ.get("SPRAY_BENCH_B200", "{}")))
+e = sp.Engine(fabrics.kv_offload(0), json.dumps({"resilience": {"degradation_ratio": 1e9}, "b200": b200}), 0)
 e.start()
 hbm = torch.empty(blk * nb, dtype=torch.uint8, device="cuda:0")
 hbm2 = torch.zeros(blk * nb, dtype=torch.uint8, device="cuda:0")
 sp.fill_splitmix(0, hbm.data_ptr(), blk * nb, 7)
-host = torch.zeros(blk * nb, dtype=torch.uint8, pin_memory=True)
-host2 = torch.zeros(blk * nb, dtype=torch.uint8, pin_memory=True)
+hb, hb2 = sp.NumaHostBuffer(0, blk * nb), sp.NumaHostBuffer(0, blk * nb)  # as the bench: NUMA-local pools
+host, host2 = hb.tensor(), hb2.tensor()
 for sid, med, t in (("hbm", sp.Medium.DEVICE, hbm), ("hbm2", sp.Medium.DEVICE, hbm2),
                     ("host", sp.Medium.HOST, host), ("host2", sp.Medium.HOST, host2)):
     e.register_segment(sp.SegmentDescriptor(sid, med, "g0", [sp.BufferDesc(0, blk * nb, t.data_ptr())]))
