@@ -724,9 +724,9 @@ def run_b200(args):
         except Exception:
             pass
         traffic = None
-        prof = os.path.join(ROOT, "profiles", "ncu_engine_kernel_final_r01.json")
+        prof = os.path.join(ROOT, "profiles", "ncu_engine_kernel_r02.json")
         if not os.path.exists(prof):
-            prof = os.path.join(ROOT, "profiles", "ncu_engine_kernel.json")
+            prof = os.path.join(ROOT, "profiles", "ncu_engine_kernel_final_r01.json")
         if os.path.exists(prof):
             try:
                 traffic = json.load(open(prof)).get("dram_bytes_per_launch")

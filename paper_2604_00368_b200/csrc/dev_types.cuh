@@ -221,6 +221,8 @@ struct alignas(64) Control {
   // 2 first decision, 3 last decision, 4 first completion applied, 5 last completion
   // applied, 6 scheduler exit
   volatile uint64_t tl[8];
+  volatile uint64_t lat_w[8];        // b200.diag: a copy warp's last chunk (picked up, copied,
+                                     // fenced, counted) and COMPLETE's word seen / record read
   volatile uint64_t lat[8];          // b200.diag: engine ns of the last pass of each pipeline stage
                                      // (HOSTRX fetch, INGRESS block, STATE decide, EGRESS post,
                                      // PUBLISH stamp, COMPLETE gather, STATE apply, PUBLISH done)

@@ -1498,6 +1498,7 @@ void Engine::debug_words(uint64_t* out, size_t n) {
     for (int q = 0; q < 16; ++q) v.push_back(static_cast<uint64_t>(ctl_->dbg[q]));
     v.push_back(E_.launch_gen);
     for (int q = 0; q < 8; ++q) v.push_back(static_cast<uint64_t>(ctl_->lat[q]));  // words 62..69
+    for (int q = 0; q < 8; ++q) v.push_back(static_cast<uint64_t>(ctl_->lat_w[q]));  // words 70..77
   }
   for (size_t i = 0; i < n; ++i) out[i] = i < v.size() ? v[i] : 0;
 }

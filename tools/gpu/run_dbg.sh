@@ -1,0 +1,10 @@
+cd $GRAFT_REPO_ROOT
+mkdir -p gpurun_out
+python -c "import torch; torch.zeros(1, device='cuda')" > /dev/null 2>&1
+( timeout -s KILL 60 python tools/relay_fault_debug.py; echo "rc=$?" ) > gpurun_out/relay_fault_debug.log 2>&1
+timeout -s KILL 120 python tools/smallslice.py > gpurun_out/smallslice.log 2>&1
+timeout -s KILL 60 python tools/latency_stages.py > gpurun_out/latency_stages.log 2>&1
+timeout -s KILL 1000 python -m pytest tests -m gpu -q --timeout 120 -p no:cacheprovider > gpurun_out/gpu_tests.log 2>&1; echo "tests rc=$?" >> gpurun_out/gpu_tests.log
+tail -n 12 gpurun_out/relay_fault_debug.log | cut -c1-600
+tail -n 4 gpurun_out/smallslice.log; tail -n 24 gpurun_out/latency_stages.log
+echo "=== tests"; grep -E "passed|failed|FAILED|Error|rc=" gpurun_out/gpu_tests.log | tail -n 15

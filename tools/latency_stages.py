@@ -28,16 +28,21 @@ e.register_segment(sp.SegmentDescriptor("d", sp.Medium.DEVICE, "b", [sp.BufferDe
 reqs = [sp.TransferRequest("s", 4096 * i, "d", 4096 * i, 4096) for i in range(64)]
 e.batch_latency_ns(reqs, 1, 50)
 deltas, tot = [], []
-w = (C.c_uint64 * 72)()
+w = (C.c_uint64 * 80)()
 for k in range(200):
     t = e.batch_latency_ns(reqs, 1, 1)[0]
-    L.lib.spray_engine_debug(e._h, w, 72)
+    L.lib.spray_engine_debug(e._h, w, 80)
     lat = list(w)[62:70]
-    deltas.append([lat[i + 1] - lat[i] for i in range(7)])
+    lw = list(w)[70:75]
+    # stamp -> worker pickup -> copied -> fenced -> counted -> COMPLETE sees the word
+    deltas.append([lat[i + 1] - lat[i] for i in range(7)] +
+                  [lw[0] - lat[4], lw[1] - lw[0], lw[2] - lw[1], lw[3] - lw[2], lw[4] - lw[3]])
     tot.append(t)
 d = np.median(np.array(deltas, dtype=np.int64), axis=0)
+WSTAGES = ["stamp->worker_pickup", "pickup->copied", "copied->fenced", "fenced->counted", "counted->complete_sees"]
 out = {"round_us_median": round(float(np.median(tot)) / 1e3, 2),
-       "device_span_us": round(float(np.median([sum(x) for x in deltas])) / 1e3, 2),
-       "stage_deltas_us": {f"{STAGES[i]}->{STAGES[i + 1]}": round(float(d[i]) / 1e3, 2) for i in range(7)}}
+       "device_span_us": round(float(np.median([sum(x[:7]) for x in deltas])) / 1e3, 2),
+       "stage_deltas_us": {f"{STAGES[i]}->{STAGES[i + 1]}": round(float(d[i]) / 1e3, 2) for i in range(7)},
+       "worker_deltas_us": {WSTAGES[i]: round(float(d[7 + i]) / 1e3, 2) for i in range(5)}}
 print(json.dumps(out, indent=1), flush=True)
 os._exit(0)
