@@ -228,6 +228,9 @@ struct alignas(64) Control {
                                      // PUBLISH stamp, COMPLETE gather, STATE apply, PUBLISH done)
   volatile uint64_t dbg[16];         // diagnostic words (relay 0: hop-1 / hop-2 tickets, slots 0-3's
                                      // free rounds and descriptor stamps, exit generation)
+  volatile uint64_t prof_y[8];       // decision phases (cycles): table, broadcast, lane-0 loop,
+                                     // its decisions, its blocks, hand-back, warp-path decisions
+  volatile uint32_t resident_gen;    // launch generation whose every engine CTA is resident
 };
 
 // Telemetry window cell (telemetry.hpp:37-44 WindowCell), one per rail per window in an
@@ -398,6 +401,7 @@ struct EngineDev {
 
 // scalars persisted in EngineDev::persist between launches
 enum : int { kPRr = 0, kPWorkTail = 1, kPCompHead = 2, kPFreeTop = 3, kPParked = 4,
-             kPLastReset = 5, kPOutChunks = 6, kPOutSlices = 7, kPSlotHwm = 8, kPNum = 16 };
+             kPLastReset = 5, kPOutChunks = 6, kPOutSlices = 7, kPSlotHwm = 8,
+             kPResident = 9, kPNum = 16 };
 
 }  // namespace spray_dev

@@ -316,7 +316,7 @@ Engine::~Engine() {
     stop();
   } catch (...) {
   }
-  free_device();
+  if (!wedged_) free_device();
 }
 
 void Engine::alloc_device() {
@@ -685,11 +685,20 @@ void Engine::stop() {
   if (!started_) return;
   ctl_->stop = 1;
   std::atomic_thread_fence(std::memory_order_seq_cst);
-  cudaStreamSynchronize(stream_);
+  // bounded: a kernel that never observes the stop word leaves the engine wedged (its
+  // memory is then leaked rather than freed under a running kernel) and says so
+  auto drain = [&](cudaStream_t s) {
+    const auto t0 = std::chrono::steady_clock::now();
+    for (;;) {
+      const cudaError_t q = cudaStreamQuery(s);
+      if (q != cudaErrorNotReady) return true;
+      if (std::chrono::steady_clock::now() - t0 > std::chrono::seconds(20)) return false;
+      std::this_thread::sleep_for(std::chrono::microseconds(200));
+    }
+  };
+  bool ok = drain(stream_);
   for (RelayHost& h : relays_)
-    if (h.stream) cudaStreamSynchronize(h.stream);
-  ctl_->stop = 0;
-  ctl_->state = 0;
+    if (h.stream) ok = drain(h.stream) && ok;
   if (has_ce_) {
     ce_run_ = false;
     for (auto& t : ce_threads_)
@@ -697,6 +706,12 @@ void Engine::stop() {
     ce_threads_.clear();
   }
   started_ = false;
+  if (!ok) {
+    wedged_ = true;
+    throw EngineError("engine kernel did not stop within 20 s");
+  }
+  ctl_->stop = 0;
+  ctl_->state = 0;
 }
 
 // ------------------------------------------------------------------ kernel lifecycle
@@ -748,10 +763,22 @@ void Engine::launch() {
     sn.trace_on = ctl_->trace_on;
   }
   CK(spray_launch::launch_engine(E_, grid, opts_.block, stream_));
+  bool local_relay = false;
+  for (const RelayHost& h : relays_) local_relay |= h.via == device_;
+  if (local_relay) {  // forwarders beside the engine start only once every engine CTA has
+    const auto t0 = std::chrono::steady_clock::now();
+    while (ctl_->resident_gen != E_.launch_gen) {
+      if (std::chrono::steady_clock::now() - t0 > std::chrono::seconds(5))
+        throw EngineError("engine kernel not resident after 5 s");
+      _mm_pause();
+    }
+  }
   for (uint32_t r = 0; r < relays_.size(); ++r) {  // hop 2 on each relay GPU
     CK(cudaSetDevice(relays_[r].via));
     int sms = 0;
     CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, relays_[r].via));
+    // beside this engine: the SMs launch_grid() left free, two forwarder CTAs each
+    if (relays_[r].via == device_) sms = std::max(2, 2 * (sms - grid));
     CK(cudaMemsetAsync(E_.relays[r].head, 0, sizeof(unsigned long long), relays_[r].stream));
     CK(spray_launch::launch_relay_forward(E_, r, sms, relays_[r].stream));
   }
@@ -1499,6 +1526,7 @@ void Engine::debug_words(uint64_t* out, size_t n) {
     v.push_back(E_.launch_gen);
     for (int q = 0; q < 8; ++q) v.push_back(static_cast<uint64_t>(ctl_->lat[q]));  // words 62..69
     for (int q = 0; q < 8; ++q) v.push_back(static_cast<uint64_t>(ctl_->lat_w[q]));  // words 70..77
+    for (int q = 0; q < 8; ++q) v.push_back(static_cast<uint64_t>(ctl_->prof_y[q]));  // words 78..85
   }
   for (size_t i = 0; i < n; ++i) out[i] = i < v.size() ? v[i] : 0;
 }

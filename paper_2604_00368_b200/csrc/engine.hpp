@@ -177,6 +177,7 @@ class Engine {
   std::map<std::string, uint32_t> set_cache_;
   std::vector<std::vector<LocalCandidate>> sets_;
   bool started_ = false;
+  bool wedged_ = false;  // stop() timed out: device memory is left to process teardown
 
   // device resources
   cudaStream_t stream_ = nullptr, copy_stream_ = nullptr;

@@ -1,0 +1,7 @@
+cd $GRAFT_REPO_ROOT
+mkdir -p gpurun_out
+python -c "import torch; torch.zeros(1, device='cuda')" > /dev/null 2>&1
+timeout -s KILL 120 python tools/smallslice.py > gpurun_out/smallslice.log 2>&1
+timeout -s KILL 1000 python -m pytest tests -m gpu -q --timeout 120 -p no:cacheprovider > gpurun_out/gpu_tests.log 2>&1; echo "tests rc=$?" >> gpurun_out/gpu_tests.log
+tail -n 4 gpurun_out/smallslice.log
+echo "=== tests"; grep -E "passed|failed|FAILED|Error|rc=" gpurun_out/gpu_tests.log | tail -n 25

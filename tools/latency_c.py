@@ -28,7 +28,8 @@ def summary(ns):
 out = {}
 dev = 0
 nb, blk = 4096, 64 << 10
-cfg = json.dumps({"resilience": {"degradation_ratio": 1e9}, "b200": {"chunk_bytes": 65536}})
+b200 = {"chunk_bytes": 65536, **json.loads(os.environ.get("LAT_B200", "{}"))}  # LAT_B200: extra engine knobs
+cfg = json.dumps({"resilience": {"degradation_ratio": 1e9}, "b200": b200})
 e = sp.Engine(fabrics.kv_offload(dev, sm_rails=1), cfg, dev)
 e.start()
 hbm = torch.empty(nb * blk, dtype=torch.uint8, device="cuda:0")

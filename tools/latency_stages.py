@@ -17,20 +17,42 @@ from paper_2604_00368_b200 import _lib as L, fabrics  # noqa: E402
 
 STAGES = ["hostrx_fetch", "ingress_block", "state_decide", "egress_post", "publish_stamp", "complete_gather",
           "state_apply", "publish_done"]
-n = 1 << 20
-e = sp.Engine(fabrics.two_node(1, 1e9, backend="cuda"),
-              json.dumps({"resilience": {"degradation_ratio": 1e9}, "b200": {"diag": True}}), 0)
-e.start()
-src = torch.empty(n, dtype=torch.uint8, device="cuda:0")
-dst = torch.zeros(n, dtype=torch.uint8, device="cuda:0")
-e.register_segment(sp.SegmentDescriptor("s", sp.Medium.DEVICE, "a", [sp.BufferDesc(0, n, src.data_ptr())]))
-e.register_segment(sp.SegmentDescriptor("d", sp.Medium.DEVICE, "b", [sp.BufferDesc(0, n, dst.data_ptr())]))
-reqs = [sp.TransferRequest("s", 4096 * i, "d", 4096 * i, 4096) for i in range(64)]
-e.batch_latency_ns(reqs, 1, 50)
+# usage: latency_stages.py [4k|kv]; LAT_B200='{"worker_fence": "gpu"}' adds engine knobs
+mode = sys.argv[1] if len(sys.argv) > 1 else "4k"
+b200 = {"diag": True, **json.loads(os.environ.get("LAT_B200", "{}"))}
+cfg = json.dumps({"resilience": {"degradation_ratio": 1e9}, "b200": {"chunk_bytes": 65536, **b200}})
+if mode == "kv":  # 32 offloads HBM -> host + 32 reloads host -> HBM, 64 KiB each (latency_c.py's batch)
+    nb, blk = 1024, 64 << 10
+    e = sp.Engine(fabrics.kv_offload(0, sm_rails=1), cfg, 0)
+    e.start()
+    bufs = {"hbm": torch.empty(nb * blk, dtype=torch.uint8, device="cuda:0"),
+            "hbm2": torch.zeros(nb * blk, dtype=torch.uint8, device="cuda:0"),
+            "host": torch.zeros(nb * blk, dtype=torch.uint8, pin_memory=True),
+            "host2": torch.zeros(nb * blk, dtype=torch.uint8, pin_memory=True)}
+    for sid, t in bufs.items():
+        e.register_segment(sp.SegmentDescriptor(sid, sp.Medium.DEVICE if sid.startswith("hbm") else sp.Medium.HOST,
+                                                "g0", [sp.BufferDesc(0, nb * blk, t.data_ptr())]))
+    rng = np.random.default_rng(1)
+    p1, p2 = rng.permutation(nb), rng.permutation(nb)
+    reqs = [r for g in range(0, nb, 32)
+            for r in [sp.TransferRequest("hbm", i * blk, "host", int(p1[i]) * blk, blk) for i in range(g, g + 32)] +
+            [sp.TransferRequest("host2", int(p2[i]) * blk, "hbm2", i * blk, blk) for i in range(g, g + 32)]]
+    per = 64
+else:
+    n = 1 << 20
+    e = sp.Engine(fabrics.two_node(1, 1e9, backend="cuda"), cfg, 0)
+    e.start()
+    src = torch.empty(n, dtype=torch.uint8, device="cuda:0")
+    dst = torch.zeros(n, dtype=torch.uint8, device="cuda:0")
+    e.register_segment(sp.SegmentDescriptor("s", sp.Medium.DEVICE, "a", [sp.BufferDesc(0, n, src.data_ptr())]))
+    e.register_segment(sp.SegmentDescriptor("d", sp.Medium.DEVICE, "b", [sp.BufferDesc(0, n, dst.data_ptr())]))
+    reqs = [sp.TransferRequest("s", 4096 * i, "d", 4096 * i, 4096) for i in range(64)]
+    per = 1
+e.batch_latency_ns(reqs, per, 50)
 deltas, tot = [], []
 w = (C.c_uint64 * 80)()
 for k in range(200):
-    t = e.batch_latency_ns(reqs, 1, 1)[0]
+    t = e.batch_latency_ns(reqs, per, 1)[0]
     L.lib.spray_engine_debug(e._h, w, 80)
     lat = list(w)[62:70]
     lw = list(w)[70:75]
@@ -40,7 +62,7 @@ for k in range(200):
     tot.append(t)
 d = np.median(np.array(deltas, dtype=np.int64), axis=0)
 WSTAGES = ["stamp->worker_pickup", "pickup->copied", "copied->fenced", "fenced->counted", "counted->complete_sees"]
-out = {"round_us_median": round(float(np.median(tot)) / 1e3, 2),
+out = {"mode": mode, "b200": b200, "round_us_median": round(float(np.median(tot)) / 1e3, 2),
        "device_span_us": round(float(np.median([sum(x[:7]) for x in deltas])) / 1e3, 2),
        "stage_deltas_us": {f"{STAGES[i]}->{STAGES[i + 1]}": round(float(d[i]) / 1e3, 2) for i in range(7)},
        "worker_deltas_us": {WSTAGES[i]: round(float(d[7 + i]) / 1e3, 2) for i in range(5)}}

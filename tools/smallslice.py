@@ -20,9 +20,11 @@ NAMES = ["host_tail", "sub_tail", "sub_head", "state", "now", "disp", "term", "f
 
 
 def dbg(k):
-    w = (C.c_uint64 * 48)()
-    L.lib.spray_engine_debug(k._h, w, 48)
-    return dict(zip(NAMES, list(w)))
+    w = (C.c_uint64 * 86)()
+    L.lib.spray_engine_debug(k._h, w, 86)
+    d = dict(zip(NAMES, list(w)))
+    d["dy"] = list(w)[78:86]
+    return d
 
 
 blk = int(os.environ.get("BLK_KIB", "64")) << 10
@@ -54,6 +56,12 @@ for rails in (1, 2, 4):
         row = {"rails": rails, "chunk": chunk, "gbs": round(gbs, 1), "ms": round(best, 4),
                "slices_per_s_M": round(nb / (best * 1e-3) / 1e6, 2), "entries": d["entries"], "loops": d["loops"]}
         row.update({kk + "_ms": round(d[kk] / ghz * 1e3, 3) for kk in keys})
+        dy = d["dy"]  # table, broadcast, lane-0 loop cycles; its decisions, blocks; hand-back; warp-path decisions
+        row["dec_split"] = {"table_cyc_per_blk": round(dy[0] / max(1, dy[4] or 1), 1),
+                            "bcast_cyc_per_blk": round(dy[1] / max(1, dy[4]), 1),
+                            "loop_cyc_per_dec": round(dy[2] / max(1, dy[3]), 1),
+                            "handback_cyc_per_blk": round(dy[5] / max(1, dy[4]), 1),
+                            "scalar_blocks": dy[4], "scalar_decisions": dy[3], "warp_decisions": dy[6]}
         print(json.dumps(row), flush=True)
         out[f"r{rails}_c{chunk}"] = row
         assert torch.equal(dst.view(nb, blk)[torch.as_tensor(perm)], src.view(nb, blk))
