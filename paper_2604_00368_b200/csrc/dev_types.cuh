@@ -374,7 +374,7 @@ struct EngineDev {
   uint32_t fence_batch;                        // chunks a copy warp moves per system fence (1..4)
   uint32_t diag;                               // write the per-stage timeline words (Control::lat)
   uint32_t worker_fence_sys;                   // copy warps fence at system scope (else GPU scope)
-  uint32_t pad_wf_;
+  uint32_t copy_bulk;                          // copy warps use the bulk-copy (TMA) pipeline
   uint64_t timeout_scan_ns;                    // deadline scan period of the TIMER warp
   uint64_t probe_interval, probe_bytes;        // resilience.hpp:23-26
   double probe_backoff_mult;

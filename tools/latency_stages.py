@@ -66,5 +66,17 @@ out = {"mode": mode, "b200": b200, "round_us_median": round(float(np.median(tot)
        "device_span_us": round(float(np.median([sum(x[:7]) for x in deltas])) / 1e3, 2),
        "stage_deltas_us": {f"{STAGES[i]}->{STAGES[i + 1]}": round(float(d[i]) / 1e3, 2) for i in range(7)},
        "worker_deltas_us": {WSTAGES[i]: round(float(d[7 + i]) / 1e3, 2) for i in range(5)}}
+tot_a = np.array(tot)
+if mode == "kv":  # rounds split at the median: where the slow ones lose their time
+    arr = np.array(deltas, dtype=np.int64)
+    med = np.median(tot_a)
+    for name, sel in (("fast_rounds", tot_a <= med), ("slow_rounds", tot_a > med)):
+        if sel.any():
+            dd = np.median(arr[sel], axis=0)
+            out[name] = {"n": int(sel.sum()), "round_us": round(float(np.median(tot_a[sel])) / 1e3, 2),
+                         "stage_deltas_us": {f"{STAGES[i]}->{STAGES[i + 1]}": round(float(dd[i]) / 1e3, 2) for i in range(7)},
+                         "worker_deltas_us": {WSTAGES[i]: round(float(dd[7 + i]) / 1e3, 2) for i in range(5)}}
+    out["round_us_hist"] = np.histogram(tot_a / 1e3, bins=8)[0].tolist()
+    out["round_us_edges"] = [round(float(x), 1) for x in np.histogram(tot_a / 1e3, bins=8)[1]]
 print(json.dumps(out, indent=1), flush=True)
 os._exit(0)
