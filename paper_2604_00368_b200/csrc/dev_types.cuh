@@ -230,6 +230,7 @@ struct alignas(64) Control {
                                      // free rounds and descriptor stamps, exit generation)
   volatile uint64_t prof_y[8];       // decision phases (cycles): table, broadcast, lane-0 loop,
                                      // its decisions, its blocks, hand-back, warp-path decisions
+  volatile uint64_t prof_z[8];       // FEEDBACK warp: chain cycles, completions, entries
   volatile uint32_t resident_gen;    // launch generation whose every engine CTA is resident
 };
 

@@ -50,6 +50,8 @@ def engine(dev, gpus, sm_rails, ce_rails, extra_cfg=None):
     if RELAY.get("max_slices"):
         cfg["scheduler"] = {"max_slices_per_transfer": RELAY["max_slices"]}
     cfg.update(extra_cfg or {})
+    if os.environ.get("NV_B200"):  # extra engine knobs, e.g. NV_B200='{"copy": "ldg"}'
+        cfg["b200"] = {**cfg.get("b200", {}), **json.loads(os.environ["NV_B200"])}
     e = sp.Engine(fabrics.peer_fabric(gpus, sm_rails=sm_rails, ce_rails=ce_rails, bw_ce=CE_GBS * 1e9,
                                       relay_via=RELAY["via"], relay_affinity=RELAY["affinity"]),
                   json.dumps(cfg), dev)

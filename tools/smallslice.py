@@ -20,10 +20,11 @@ NAMES = ["host_tail", "sub_tail", "sub_head", "state", "now", "disp", "term", "f
 
 
 def dbg(k):
-    w = (C.c_uint64 * 86)()
-    L.lib.spray_engine_debug(k._h, w, 86)
+    w = (C.c_uint64 * 94)()
+    L.lib.spray_engine_debug(k._h, w, 94)
     d = dict(zip(NAMES, list(w)))
     d["dy"] = list(w)[78:86]
+    d["dz"] = list(w)[86:94]
     return d
 
 
@@ -62,6 +63,9 @@ for rails in (1, 2, 4):
                             "loop_cyc_per_dec": round(dy[2] / max(1, dy[3]), 1),
                             "handback_cyc_per_blk": round(dy[5] / max(1, dy[4]), 1),
                             "scalar_blocks": dy[4], "scalar_decisions": dy[3], "warp_decisions": dy[6]}
+        dz = d["dz"]
+        row["fb_split"] = {"chain_cyc_per_completion": round(dz[0] / max(1, dz[1]), 1), "completions": dz[1],
+                           "entries": dz[2], "busy_cyc_per_completion": round(d["fb_busy"] / max(1, dz[1]), 1)}
         print(json.dumps(row), flush=True)
         out[f"r{rails}_c{chunk}"] = row
         assert torch.equal(dst.view(nb, blk)[torch.as_tensor(perm)], src.view(nb, blk))
