@@ -76,6 +76,25 @@ __global__ void k2(unsigned long long* g, long long* cyc) {
   t1 = clock64(); cyc[15] = (t1 - t0) / n;
   g[6] = v;
 }
+// fence flavours, idle, after one store to a host-mapped word (the PUBLISH pattern)
+__global__ void k3(volatile unsigned int* host, long long* cyc) {
+  const int n = 64;
+  long long t0, t1;
+  unsigned long long v = 0;
+#define FENCE_CASE(idx, stmt)                                        \
+  t0 = clock64();                                                    \
+  for (int i = 0; i < n; ++i) { host[i & 7] = i; stmt; v += clock64() & 1; } \
+  t1 = clock64(); cyc[idx] = (t1 - t0) / n;
+  FENCE_CASE(0, asm volatile("fence.sc.sys;" ::: "memory"))
+  FENCE_CASE(1, asm volatile("fence.acq_rel.sys;" ::: "memory"))
+  FENCE_CASE(2, asm volatile("fence.sc.gpu;" ::: "memory"))
+  FENCE_CASE(3, asm volatile("fence.acq_rel.gpu;" ::: "memory"))
+  FENCE_CASE(4, asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(host + 8), "r"((unsigned)v) : "memory"))
+  FENCE_CASE(5, (void)0)
+  FENCE_CASE(6, asm volatile("fence.release.sys;" ::: "memory"))
+  FENCE_CASE(7, asm volatile("fence.release.gpu;" ::: "memory"))
+  host[15] = (unsigned)v;
+}
 int main() {
   double* o; long long* c; cudaMalloc(&o, 256); cudaMalloc(&c, 16 * 8);
   k<<<1, 32>>>(o, c, 1.0, 3); cudaDeviceSynchronize();
@@ -87,6 +106,18 @@ int main() {
   printf("{\"nanosleep_32\": %lld, \"nanosleep_128\": %lld, \"nanosleep_512\": %lld, \"nanosleep_2048\": %lld, "
          "\"ld_acquire_gpu\": %lld, \"atomic_add\": %lld, \"atomic_cas\": %lld, \"fence_sys_idle\": %lld}\n",
          h2[8], h2[9], h2[10], h2[11], h2[12], h2[13], h2[14], h2[15]);
+  {
+    unsigned int* hw; cudaHostAlloc(&hw, 64, cudaHostAllocMapped);
+    unsigned int* dw; cudaHostGetDevicePointer(&dw, hw, 0);
+    long long* c3; cudaMalloc(&c3, 8 * 8);
+    k3<<<1, 1>>>(dw, c3); cudaDeviceSynchronize();
+    k3<<<1, 1>>>(dw, c3); cudaDeviceSynchronize();
+    long long h3[8]; cudaMemcpy(h3, c3, 64, cudaMemcpyDeviceToHost);
+    printf("{\"after_host_store\": {\"fence_sc_sys\": %lld, \"fence_acq_rel_sys\": %lld, \"fence_sc_gpu\": %lld, "
+           "\"fence_acq_rel_gpu\": %lld, \"st_release_sys\": %lld, \"none\": %lld, \"fence_release_sys\": %lld, "
+           "\"fence_release_gpu\": %lld}}\n",
+           h3[0], h3[1], h3[2], h3[3], h3[4], h3[5], h3[6], h3[7]);
+  }
   long long h[8]; cudaMemcpy(h, c, 64, cudaMemcpyDeviceToHost);
   const char* names[8] = {"dmul", "dadd", "ddiv_rn", "redux_min", "shfl_xor_f64", "mod_u32", "ballot_popc", "dsetp_sel"};
   printf("{");
