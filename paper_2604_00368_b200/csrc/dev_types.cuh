@@ -376,6 +376,8 @@ struct EngineDev {
   uint32_t diag;                               // write the per-stage timeline words (Control::lat)
   uint32_t worker_fence_sys;                   // copy warps fence at system scope (else GPU scope)
   uint32_t copy_bulk;                          // copy warps use the bulk-copy (TMA) pipeline
+  uint32_t fence_release;                      // system fences as fence.release.sys (b200.fence)
+  uint32_t pad_fr_;
   uint64_t timeout_scan_ns;                    // deadline scan period of the TIMER warp
   uint64_t probe_interval, probe_bytes;        // resilience.hpp:23-26
   double probe_backoff_mult;

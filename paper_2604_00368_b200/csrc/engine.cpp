@@ -179,7 +179,7 @@ EngineOptions engine_options_from_json(const std::string& text) {
       const Json& b = j.at("b200");
       reject_unknown(b, {"grid", "block", "chunk_bytes", "idle_exit_ms", "slice_capacity", "work_capacity",
                          "sub_capacity", "batch_slots", "gate_timeout_ms", "post_window", "fence_batch", "diag",
-                         "no_peer", "staged_routes", "worker_fence", "copy"},
+                         "no_peer", "staged_routes", "worker_fence", "copy", "fence"},
                      "b200");
       eo.post_window = static_cast<uint32_t>(b.number_or("post_window", eo.post_window));
       eo.fence_batch = static_cast<uint32_t>(b.number_or("fence_batch", eo.fence_batch));
@@ -188,6 +188,11 @@ EngineOptions engine_options_from_json(const std::string& text) {
         const std::string wf = b.at("worker_fence").as_string();
         if (wf != "sys" && wf != "gpu") throw ConfigError("b200.worker_fence must be sys or gpu");
         eo.worker_fence_sys = wf == "sys";
+      }
+      if (b.contains("fence")) {
+        const std::string fe = b.at("fence").as_string();
+        if (fe != "release" && fe != "sc") throw ConfigError("b200.fence must be release or sc");
+        eo.fence_release = fe == "release";
       }
       if (b.contains("copy")) {
         const std::string cp = b.at("copy").as_string();
@@ -461,6 +466,7 @@ void Engine::alloc_device() {
   E_.diag = opts_.diag ? 1u : 0u;
   E_.worker_fence_sys = opts_.worker_fence_sys ? 1u : 0u;
   E_.copy_bulk = opts_.copy_bulk ? 1u : 0u;
+  E_.fence_release = opts_.fence_release ? 1u : 0u;
   // the deadline scan runs ~8 times per timeout (the reference's wheel has 10 ms buckets,
   // engine.cpp:18), bounded to [0.2, 10] ms
   E_.timeout_scan_ns = std::min<uint64_t>(10'000'000, std::max<uint64_t>(200'000, opts_.res.slice_timeout_ns / 8));

@@ -47,6 +47,7 @@ struct EngineOptions {
                                                  // its next chunk is already queued (1 = every chunk)
   bool diag = false;                             // per-stage timeline words (Control::lat)
   bool worker_fence_sys = true;                  // copy warps' fence scope before counting a chunk
+  bool fence_release = false;                    // system fences as fence.release.sys (else fence.sc.sys)
   bool copy_bulk = true;                         // copy warps move chunks with bulk copies (TMA) through
                                                  // shared memory (else 16-deep vector loads/stores)
   bool staged_routes = true;                     // synthesize host-staged routes to GPUs without peer access
