@@ -231,6 +231,7 @@ struct alignas(64) Control {
   volatile uint64_t prof_y[8];       // decision phases (cycles): table, broadcast, lane-0 loop,
                                      // its decisions, its blocks, hand-back, warp-path decisions
   volatile uint64_t prof_z[8];       // FEEDBACK warp: chain cycles, completions, entries
+  volatile uint64_t lat_s[8];        // b200.diag: STATE sub-steps (block seen, slots, set, -, completion seen, FEEDBACK done)
   volatile uint32_t resident_gen;    // launch generation whose every engine CTA is resident
 };
 

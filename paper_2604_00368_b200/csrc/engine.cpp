@@ -1540,6 +1540,7 @@ void Engine::debug_words(uint64_t* out, size_t n) {
     for (int q = 0; q < 8; ++q) v.push_back(static_cast<uint64_t>(ctl_->lat_w[q]));  // words 70..77
     for (int q = 0; q < 8; ++q) v.push_back(static_cast<uint64_t>(ctl_->prof_y[q]));  // words 78..85
     for (int q = 0; q < 8; ++q) v.push_back(static_cast<uint64_t>(ctl_->prof_z[q]));  // words 86..93
+    for (int q = 0; q < 8; ++q) v.push_back(static_cast<uint64_t>(ctl_->lat_s[q]));  // words 94..101
   }
   for (size_t i = 0; i < n; ++i) out[i] = i < v.size() ? v[i] : 0;
 }
