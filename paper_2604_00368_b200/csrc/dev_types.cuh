@@ -306,8 +306,12 @@ struct RelayDev {
   uint32_t* seq;                // this GPU's HBM (host-staged: pinned host): per-slot free round
   unsigned long long* tail;     // this GPU's HBM: hop-1 ticket counter (workers)
   unsigned long long* head;     // K's HBM: hop-2 ticket counter (forwarder warps)
-  RelayDone* done;              // host-staged only: pinned host completion ring
+  RelayDone* done;              // host-staged only: this GPU's HBM, hop 1's record of each slot's
+                                //   chunk (slice, generation, units); stamp unused
+  uint64_t* done_stamp;         // host-staged only: pinned host, per slot: (launch_gen << 32) |
+                                //   (ticket + 1) once the forwarder has drained the slot
   unsigned long long* consumed; // host-staged only: this GPU's HBM, done records HOSTRX drained
+  uint32_t* writers;            // host-staged only: this GPU's HBM, hop-1 warps writing the pool now
   uint32_t n_slots, via;        // power of two; relay GPU ordinal
   uint32_t host_staged, pad_;
 };
@@ -378,7 +382,7 @@ struct EngineDev {
   uint32_t worker_fence_sys;                   // copy warps fence at system scope (else GPU scope)
   uint32_t copy_bulk;                          // copy warps use the bulk-copy (TMA) pipeline
   uint32_t fence_release;                      // system fences as fence.release.sys (b200.fence)
-  uint32_t pad_fr_;
+  uint32_t bulk_stages;                        // shared-memory stages per copy warp (2..7)
   uint64_t timeout_scan_ns;                    // deadline scan period of the TIMER warp
   uint64_t probe_interval, probe_bytes;        // resilience.hpp:23-26
   double probe_backoff_mult;

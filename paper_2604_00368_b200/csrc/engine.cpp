@@ -179,7 +179,7 @@ EngineOptions engine_options_from_json(const std::string& text) {
       const Json& b = j.at("b200");
       reject_unknown(b, {"grid", "block", "chunk_bytes", "idle_exit_ms", "slice_capacity", "work_capacity",
                          "sub_capacity", "batch_slots", "gate_timeout_ms", "post_window", "fence_batch", "diag",
-                         "no_peer", "staged_routes", "worker_fence", "copy", "fence"},
+                         "no_peer", "staged_routes", "worker_fence", "copy", "fence", "bulk_stages"},
                      "b200");
       eo.post_window = static_cast<uint32_t>(b.number_or("post_window", eo.post_window));
       eo.fence_batch = static_cast<uint32_t>(b.number_or("fence_batch", eo.fence_batch));
@@ -189,6 +189,8 @@ EngineOptions engine_options_from_json(const std::string& text) {
         if (wf != "sys" && wf != "gpu") throw ConfigError("b200.worker_fence must be sys or gpu");
         eo.worker_fence_sys = wf == "sys";
       }
+      eo.bulk_stages = static_cast<uint32_t>(b.number_or("bulk_stages", eo.bulk_stages));
+      if (eo.bulk_stages < 2 || eo.bulk_stages > 7) throw ConfigError("b200.bulk_stages must be in [2, 7]");
       if (b.contains("fence")) {
         const std::string fe = b.at("fence").as_string();
         if (fe != "release" && fe != "sc") throw ConfigError("b200.fence must be release or sc");
@@ -394,7 +396,9 @@ void Engine::alloc_device() {
       const uint32_t warps = static_cast<uint32_t>(std::max(1, launch_grid() - 1)) * (opts_.block / 32);
       uint32_t w = opts_.post_window ? opts_.post_window
                                      : (r.executor == 1 ? 2048u : std::max(64u, 2 * (opts_.fence_batch + 1) * warps));
-      if (r.host_staged && !opts_.post_window) w = 2048;  // the staging pool's slots
+      // host-staged relays: the staging pool's slots (the forwarder's PCIe reads take
+      // hundreds of µs under load, so the whole pool is kept in flight)
+      if (r.host_staged && !opts_.post_window) w = 2048;
       rd[i].window = r.executor == 1 ? std::min<uint32_t>(w, ce_cap / 2) : w;
     }
     rd[i].bandwidth = r.bandwidth;
@@ -467,6 +471,7 @@ void Engine::alloc_device() {
   E_.worker_fence_sys = opts_.worker_fence_sys ? 1u : 0u;
   E_.copy_bulk = opts_.copy_bulk ? 1u : 0u;
   E_.fence_release = opts_.fence_release ? 1u : 0u;
+  E_.bulk_stages = opts_.bulk_stages;
   // the deadline scan runs ~8 times per timeout (the reference's wheel has 10 ms buckets,
   // engine.cpp:18), bounded to [0.2, 10] ms
   E_.timeout_scan_ns = std::min<uint64_t>(10'000'000, std::max<uint64_t>(200'000, opts_.res.slice_timeout_ns / 8));
@@ -607,7 +612,7 @@ void Engine::setup_relay(uint32_t idx, int via, bool host_staged) {
     R.desc = static_cast<RelayDesc*>(pinned(sizeof(RelayDesc) * kSlots));
     R.exit_gen = static_cast<uint32_t*>(pinned(sizeof(uint32_t)));
     R.seq = static_cast<uint32_t*>(pinned(sizeof(uint32_t) * kSlots));
-    R.done = static_cast<RelayDone*>(pinned(sizeof(RelayDone) * kSlots));
+    R.done_stamp = static_cast<uint64_t*>(pinned(sizeof(uint64_t) * kSlots));
   } else {
     R.staging = static_cast<uint8_t*>(on_via(size_t(kSlots) << E_.chunk_shift));
     R.desc = static_cast<RelayDesc*>(on_via(sizeof(RelayDesc) * kSlots));
@@ -625,6 +630,14 @@ void Engine::setup_relay(uint32_t idx, int via, bool host_staged) {
     CK(cudaMemset(p, 0, sizeof(unsigned long long)));
     dev_allocs_.push_back(p);
     R.consumed = static_cast<unsigned long long*>(p);
+    CK(cudaMalloc(&p, sizeof(RelayDone) * kSlots));
+    CK(cudaMemset(p, 0, sizeof(RelayDone) * kSlots));
+    dev_allocs_.push_back(p);
+    R.done = static_cast<RelayDone*>(p);
+    CK(cudaMalloc(&p, sizeof(uint32_t)));
+    CK(cudaMemset(p, 0, sizeof(uint32_t)));
+    dev_allocs_.push_back(p);
+    R.writers = static_cast<uint32_t*>(p);
   }
   CK(cudaMalloc(&p, sizeof(unsigned long long)));
   CK(cudaMemset(p, 0, sizeof(unsigned long long)));

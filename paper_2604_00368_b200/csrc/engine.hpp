@@ -48,6 +48,7 @@ struct EngineOptions {
   bool diag = false;                             // per-stage timeline words (Control::lat)
   bool worker_fence_sys = true;                  // copy warps' fence scope before counting a chunk
   bool fence_release = false;                    // system fences as fence.release.sys (else fence.sc.sys)
+  uint32_t bulk_stages = 4;                      // shared-memory stages per copy warp (4 KiB each)
   bool copy_bulk = true;                         // copy warps move chunks with bulk copies (TMA) through
                                                  // shared memory (else 16-deep vector loads/stores)
   bool staged_routes = true;                     // synthesize host-staged routes to GPUs without peer access

@@ -17,9 +17,9 @@ sm = int(sys.argv[2]) if len(sys.argv) > 2 else 0
 grid = int(sys.argv[3]) if len(sys.argv) > 3 else 0
 topo = fabrics.peer_fabric([0, 1], sm_rails=sm, relay_via=[via], relay_affinity="direct")
 print(json.dumps(json.loads(topo)["rails"]), flush=True)
-cfg = {"resilience": {"degradation_ratio": 1e9, "slice_timeout_ms": 500}}
+cfg = {"resilience": {"degradation_ratio": 1e9, "slice_timeout_ms": 500}, "b200": {"diag": True}}
 if grid:
-    cfg["b200"] = {"grid": grid}
+    cfg["b200"]["grid"] = grid
 e = sp.Engine(topo, json.dumps(cfg), 0)
 e.start()
 n = 8 << 20

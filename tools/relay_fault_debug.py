@@ -23,7 +23,7 @@ def mark(*a):
 
 mark("start", n)
 e = sp.Engine(fabrics.peer_fabric([0, 1], sm_rails=1, relay_via=[0]),
-              json.dumps({"resilience": {"degradation_ratio": 1e9}}), 0)
+              json.dumps({"resilience": {"degradation_ratio": 1e9}, "b200": {"diag": True}}), 0)
 e.start()
 mark("engine started")
 src = torch.empty(n, dtype=torch.uint8, device="cuda:0")

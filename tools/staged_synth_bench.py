@@ -19,6 +19,7 @@ from paper_2604_00368_b200 import fabrics  # noqa: E402
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--reps", type=int, default=5)
+ap.add_argument("--mib", type=int, nargs="*", default=[64, 256, 1024])
 args = ap.parse_args()
 assert torch.cuda.device_count() >= 2, "needs 2 GPUs"
 cfg = {"resilience": {"degradation_ratio": 1e9}, "b200": {"no_peer": [1], **json.loads(os.environ.get("ST_B200", "{}"))}}
@@ -32,7 +33,7 @@ sp.fill_splitmix(0, src.data_ptr(), big, 51)
 dst = torch.zeros(big, dtype=torch.uint8, device="cuda:1")
 e.register_segment(sp.SegmentDescriptor("s", sp.Medium.DEVICE, "g0", [sp.BufferDesc(0, big, src.data_ptr())]))
 e.register_segment(sp.SegmentDescriptor("d", sp.Medium.DEVICE, "g1", [sp.BufferDesc(0, big, dst.data_ptr())]))
-for n in (64 << 20, 256 << 20, big):
+for n in [m << 20 for m in args.mib]:
     best = None
     for _ in range(args.reps):
         b = e.allocate_batch()
@@ -47,6 +48,16 @@ for n in (64 << 20, 256 << 20, big):
     out[f"{n >> 20}MiB"] = {"gbs": round(n / best / 1e9, 2), "ms": round(best * 1e3, 3), "bit_exact": bool(exact)}
     print(json.dumps({f"{n >> 20}MiB": out[f"{n >> 20}MiB"]}), flush=True)
 out["bytes_by_rail"] = {e.rail_id(r): e.rail_stats(r).bytes_ok for r in range(e.rail_count())}
+if json.loads(os.environ.get("ST_B200", "{}")).get("diag"):
+    import ctypes as C
+    from paper_2604_00368_b200 import _lib as L
+    w = (C.c_uint64 * 62)()
+    L.lib.spray_engine_debug(e._h, w, 62)
+    d = list(w)[45:61]
+    out["diag"] = {"hostrx_staged_reads": d[0], "hostrx_read_cycles_avg": d[1] / max(1, d[0]), "hostrx_read_cycles_max": d[2],
+                   "fwd_tickets": d[4], "fwd_wait_ns_avg": d[5] / max(1, d[4]), "fwd_wait_ns_max": d[7],
+                   "fwd_copy_ns_avg": d[6] / max(1, d[4])}
+    print(json.dumps(out["diag"]), flush=True)
 e.stop()
 os.makedirs("gpurun_out", exist_ok=True)
 json.dump(out, open("gpurun_out/staged_synth.json", "w"), indent=1)
