@@ -56,7 +56,8 @@ if json.loads(os.environ.get("ST_B200", "{}")).get("diag"):
     d = list(w)[45:61]
     out["diag"] = {"hostrx_staged_reads": d[0], "hostrx_read_cycles_avg": d[1] / max(1, d[0]), "hostrx_read_cycles_max": d[2],
                    "fwd_tickets": d[4], "fwd_wait_ns_avg": d[5] / max(1, d[4]), "fwd_wait_ns_max": d[7],
-                   "fwd_copy_ns_avg": d[6] / max(1, d[4])}
+                   "fwd_copy_ns_avg": d[6] / max(1, d[4]), "hop1_chunks": d[8], "hop1_copy_fence_ns_avg": d[9] / max(1, d[8]),
+                   "hop1_wait_ns_avg": d[10] / max(1, d[8])}
     print(json.dumps(out["diag"]), flush=True)
 e.stop()
 os.makedirs("gpurun_out", exist_ok=True)
