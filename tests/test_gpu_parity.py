@@ -153,6 +153,45 @@ def test_live_trace_replays_identically(co, policy):
     e.stop()
 
 
+@pytest.mark.parametrize("policy", ["telemetry", "rr", "hash"])
+def test_live_trace_many_candidates_and_uniform_blocks_replay_identically(co, policy):
+    """The decision paths by candidate count: 2 and 3 rails (the lane-0 scalar loop over
+    per-block score tables) and 8 rails (the warp loop), each fed both uniform 32-slice
+    blocks (one-slice intents of one length) and ragged multi-slice intents."""
+    for n_rails in (2, 3, 8):
+        bws = [float(4e9 / (1 + (i % 3))) for i in range(n_rails)]
+        topo = fabrics.two_node(n_rails, bws, backend="cuda")
+        sc = sched_config(policy={"telemetry": 0, "rr": 1, "hash": 2}[policy])
+        e = make_engine(topo, {"scheduler": {"policy": policy}, "resilience": {"degradation_ratio": 1e9},
+                               "b200": {"chunk_bytes": 65536}})
+        e.trace_enable(1 << 18)
+        n = 64 << 20
+        src = dev_buf(n, fill_seed=7 + n_rails)
+        dst = dev_buf(n)
+        e.register_segment(sp.SegmentDescriptor("s", sp.Medium.DEVICE, "a", [sp.BufferDesc(0, n, src.data_ptr())]))
+        e.register_segment(sp.SegmentDescriptor("d", sp.Medium.DEVICE, "b", [sp.BufferDesc(0, n, dst.data_ptr())]))
+        rng = np.random.default_rng(23 + n_rails)
+        for k in range(4):
+            b = e.allocate_batch()
+            if k % 2 == 0:  # uniform: 256 one-slice intents of 64 KiB at random offsets
+                reqs = [sp.TransferRequest("s", int(o) * 65536, "d", int(o) * 65536, 65536)
+                        for o in rng.permutation(n // 65536)[:256]]
+            else:
+                reqs = []
+                for _ in range(8):
+                    ln = int(rng.integers(1, 6 << 20))
+                    off = int(rng.integers(0, n - ln))
+                    reqs.append(sp.TransferRequest("s", off, "d", off, ln))
+            e.submit_transfers(b, reqs)
+            assert e.await_batch(b, 30_000_000_000).state == sp.BatchState.COMPLETE
+            e.free_batch(b)
+        torch.cuda.synchronize()
+        bw, tier, rank = rails_of(topo)
+        ev, dec = replay_live(co, e, sc, res_config(degradation_ratio=1e9), bw, tier, rank)
+        assert len(dec) > 500 and (ev["kind"] == 2).sum() == len(dec)
+        e.stop()
+
+
 def test_live_trace_with_degradation_exclusions_replays_identically(co):
     """Tight degradation settings so rails are excluded by observe() on OK completions
     (the completion fast path's lane-parallel classification) and reintegrated by probes;
