@@ -57,20 +57,22 @@ for k in range(200):
     lat = list(w)[62:70]
     lw = list(w)[70:75]
     # stamp -> worker pickup -> copied -> fenced -> counted -> COMPLETE sees the word
-    ls = list(w)[94:100]
+    ls = list(w)[94:102]
     deltas.append([lat[i + 1] - lat[i] for i in range(7)] +
                   [lw[0] - lat[4], lw[1] - lw[0], lw[2] - lw[1], lw[3] - lw[2], lw[4] - lw[3]] +
-                  [ls[0] - lat[1], ls[1] - ls[0], ls[2] - ls[1], lat[2] - ls[2], ls[4] - lat[5], ls[5] - ls[4], lat[6] - ls[5]])
+                  [ls[0] - lat[1], ls[1] - ls[0], ls[2] - ls[1], lat[2] - ls[2], ls[4] - lat[5], ls[5] - ls[4], lat[6] - ls[5],
+                   ls[3] - ls[5], ls[6] - ls[3], ls[7] - ls[6], lat[6] - ls[7]])
     tot.append(t)
 d = np.median(np.array(deltas, dtype=np.int64), axis=0)
 SSTAGES = ["ingress_block->state_sees_block", "sees_block->slots_reserved", "slots->set_loaded", "set->decided",
-           "complete_gather->state_sees_entry", "sees_entry->feedback_done", "feedback_done->applied"]
+           "complete_gather->state_sees_entry", "sees_entry->feedback_done", "feedback_done->applied",
+           "  apply: fb_done->prologue_done", "  apply: prologue->lead_done", "  apply: lead->slots_freed", "  apply: freed->end"]
 WSTAGES = ["stamp->worker_pickup", "pickup->copied", "copied->fenced", "fenced->counted", "counted->complete_sees"]
 out = {"mode": mode, "b200": b200, "round_us_median": round(float(np.median(tot)) / 1e3, 2),
        "device_span_us": round(float(np.median([sum(x[:7]) for x in deltas])) / 1e3, 2),
        "stage_deltas_us": {f"{STAGES[i]}->{STAGES[i + 1]}": round(float(d[i]) / 1e3, 2) for i in range(7)},
        "worker_deltas_us": {WSTAGES[i]: round(float(d[7 + i]) / 1e3, 2) for i in range(5)},
-       "state_deltas_us": {SSTAGES[i]: round(float(d[12 + i]) / 1e3, 2) for i in range(7)}}
+       "state_deltas_us": {SSTAGES[i]: round(float(d[12 + i]) / 1e3, 2) for i in range(11)}}
 tot_a = np.array(tot)
 if mode == "kv":  # rounds split at the median: where the slow ones lose their time
     arr = np.array(deltas, dtype=np.int64)
