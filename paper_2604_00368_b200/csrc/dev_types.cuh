@@ -58,10 +58,11 @@ struct RailState {
   uint32_t hist[48];
 };
 
+constexpr uint32_t kNoSet = 0xffffffffu;
 // Candidate set (orchestrator.cpp:39-81 output), flattened for the device.
 struct alignas(16) CandSet {
   uint32_t n_locals;
-  uint32_t pad_;
+  uint32_t next_set;  // the plan's next route (TransferPlan::advance_past_backend), kNoSet if none
   uint32_t local[kMaxLocals];
   uint32_t n_pairs[kMaxLocals];
   uint32_t pair_remote[kMaxLocals][kMaxPairs];

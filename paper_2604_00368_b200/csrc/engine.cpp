@@ -911,11 +911,35 @@ uint32_t Engine::set_for(const Segment& src, const Segment& dst, Direction dir) 
   if (it != set_cache_.end()) return it->second;
   CK(cudaSetDevice(device_));
   auto routes = build_plan(topo_, src, dst, dir, opts_.sched.penalty, caps_);  // throws NoRouteError
-  Route r = routes.front();
-  filter_staged(r, src, dst);
+  // The plan's routes in order (one per backend chain, build_plan's order). The first is
+  // the active route; each set names the next, which a slice moves to once its attempts
+  // on a route are exhausted (substitute_or_fail, engine.cpp:676-683).
+  std::vector<Route> plan;
+  for (size_t k = 0; k < routes.size(); ++k) {
+    Route r = routes[k];
+    if (k == 0) {
+      filter_staged(r, src, dst);  // throws NoRouteError for the active route
+    } else {
+      try {
+        filter_staged(r, src, dst);
+      } catch (const NoRouteError&) {
+        continue;
+      }
+    }
+    plan.push_back(std::move(r));
+  }
+  if (sets_.size() + plan.size() > opts_.max_sets) throw EngineError("candidate-set table full");
+  const uint32_t first = static_cast<uint32_t>(sets_.size());
+  for (size_t k = 0; k < plan.size(); ++k)
+    add_set(plan[k], k + 1 < plan.size() ? first + static_cast<uint32_t>(k + 1) : kNoSet);
+  set_cache_.emplace(key, first);
+  return first;
+}
+
+uint32_t Engine::add_set(const Route& r, uint32_t next) {
   if (r.candidates.size() > size_t(kMaxLocals)) throw ConfigError("route has more than 32 local rails");
-  if (sets_.size() >= opts_.max_sets) throw EngineError("candidate-set table full");
   CandSet cs{};
+  cs.next_set = next;
   cs.n_locals = static_cast<uint32_t>(r.candidates.size());
   for (size_t l = 0; l < r.candidates.size(); ++l) {
     const LocalCandidate& c = r.candidates[l];
@@ -934,7 +958,6 @@ uint32_t Engine::set_for(const Segment& src, const Segment& dst, Direction dir) 
     CK(cudaStreamSynchronize(copy_stream_));
   }
   sets_.push_back(r.candidates);
-  set_cache_.emplace(key, id);
   return id;
 }
 

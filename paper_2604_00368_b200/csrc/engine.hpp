@@ -156,6 +156,7 @@ class Engine {
   int launch_grid();
   void ensure_running();
   uint32_t set_for(const Segment& src, const Segment& dst, Direction dir);
+  uint32_t add_set(const Route& r, uint32_t next);  // one route's candidate set, chained to the plan's next
   void translate(SegRec& s);
   void publish(const spray_dev::Intent* in, size_t n);
   SegRec& seg_lookup(const char* name, const char*& cname, SegRec*& crec);

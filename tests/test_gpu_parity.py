@@ -655,6 +655,44 @@ def test_attempts_exhausted_fails_batch_with_all_routes_exhausted():
     e.stop()
 
 
+def test_backend_substitution_after_exhausted_attempts(co):
+    """substitute_or_fail / advance_past_backend / reissue (engine.cpp:676-761,
+    orchestrator.cpp:20-33): the plan holds two routes, backend "cuda" (active, better
+    tier) and backend "memory". Every rail of the active route is DOWN for the whole run;
+    each slice exhausts its attempts there, moves to the next route, is decided there with
+    the model and completes. Bit-exact, no failed batch, and the live trace (with the
+    decisions on the second route's candidate set) replays identically."""
+    doc = json.loads(fabrics.two_node(2, 1e9, backend="cuda"))
+    for n_ in ("a", "b"):
+        doc["rails"].append({"id": f"{n_}.m0", "node": n_, "bandwidth_bytes_per_sec": 5e8,
+                             "affinity": "same_socket", "backend": "memory"})
+    topo = json.dumps(doc)
+    e = make_engine(topo, {"backends": ["cuda", "memory"],
+                           "resilience": {"degradation_ratio": 1e9, "max_attempts": 2, "failure_threshold": 1000}})
+    e.trace_enable(1 << 16)
+    n = 8 << 20
+    src, dst = dev_buf(n, 12), dev_buf(n)
+    e.register_segment(sp.SegmentDescriptor("s", sp.Medium.DEVICE, "a", [sp.BufferDesc(0, n, src.data_ptr())]))
+    e.register_segment(sp.SegmentDescriptor("d", sp.Medium.DEVICE, "b", [sp.BufferDesc(0, n, dst.data_ptr())]))
+    for r in ("a.r0", "a.r1"):
+        e.inject_fault(r, sp.FaultEffect.DOWN, 0, 1 << 62)
+    b = e.allocate_batch()
+    e.submit_transfer(b, sp.TransferRequest("s", 0, "d", 0, n))
+    st = e.await_batch(b, 30_000_000_000)
+    assert st.state == sp.BatchState.COMPLETE, st
+    assert sp.checksum(DEV, dst.data_ptr(), n) == sp.checksum(DEV, src.data_ptr(), n)
+    assert e.counters()["batches_failed"] == 0
+    by = {e.rail_id(r): e.rail_stats(r).bytes_ok for r in range(e.rail_count())}
+    assert by["a.m0"] == n and by["a.r0"] == 0 and by["a.r1"] == 0
+    assert int(e.trace_candidates()[0]) >= 2  # both routes of the plan are candidate sets
+    bw, tier, rank = rails_of(topo)
+    ev, dec = replay_live(co, e, sched_config(), res_config(degradation_ratio=1e9, max_attempts=2,
+                                                             failure_threshold=1000), bw, tier, rank)
+    assert (ev["kind"] == 1).sum() == len(dec) > 0
+    e.free_batch(b)
+    e.stop()
+
+
 # ------------------------------------------------------------------ copy-engine rails
 def test_copy_engine_rail_bit_exact():
     topo = fabrics.kv_offload(DEV, sm_rails=1, ce_rails=1)
