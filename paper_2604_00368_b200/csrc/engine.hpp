@@ -46,7 +46,8 @@ struct EngineOptions {
   uint32_t fence_batch = 2;                      // chunks a copy warp copies per system fence when
                                                  // its next chunk is already queued (1 = every chunk)
   bool diag = false;                             // per-stage timeline words (Control::lat)
-  bool worker_fence_sys = true;                  // copy warps' fence scope before counting a chunk
+  bool worker_fence_sys = false;                 // copy warps fence at GPU scope before counting a chunk; PUBLISH's
+                                                 // system fence before the host-visible words is cumulative over them
   bool fence_release = false;                    // system fences as fence.release.sys (else fence.sc.sys)
   uint32_t bulk_stages = 4;                      // shared-memory stages per copy warp (4 KiB each)
   bool copy_bulk = true;                         // copy warps move chunks with bulk copies (TMA) through

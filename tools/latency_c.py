@@ -47,7 +47,11 @@ d2h = [sp.TransferRequest("hbm", int(p1[i]) * blk, "host", i * blk, 4096) for i 
 off = [sp.TransferRequest("hbm", i * blk, "host", int(p1[i]) * blk, blk) for i in range(nb)]
 on = [sp.TransferRequest("host2", int(p2[i]) * blk, "hbm2", i * blk, blk) for i in range(nb)]
 kv = [r for g in range(0, nb, 32) for r in off[g:g + 32] + on[g:g + 32]]
-for name, reqs, per in (("intent_4k_hbm2hbm", d2d, 1), ("intent_4k_hbm2host", d2h, 1), ("kv_64x64k", kv, 64)):
+kv_rf = [r for g in range(0, nb, 32) for r in on[g:g + 32] + off[g:g + 32]]  # the reloads first in each batch
+cases = [("intent_4k_hbm2hbm", d2d, 1), ("intent_4k_hbm2host", d2h, 1), ("kv_64x64k", kv, 64)]
+if os.environ.get("LAT_KV_REVERSED"):
+    cases.append(("kv_64x64k_reloads_first", kv_rf, 64))
+for name, reqs, per in cases:
     e.batch_latency_ns(reqs, per, 50)  # warm
     out[name] = summary(e.batch_latency_ns(reqs, per, 1000))
     print(name, json.dumps(out[name]), flush=True)
