@@ -1,0 +1,12 @@
+# final 2-GPU session on the round's last build
+cd $GRAFT_REPO_ROOT
+mkdir -p gpurun_out
+python -c "import torch; torch.zeros(1, device='cuda')" > /dev/null 2>&1
+timeout -s KILL 900 python -m pytest tests -m gpu -q --timeout 150 -p no:cacheprovider > gpurun_out/gpu_tests_n2.log 2>&1; echo "rc=$?" >> gpurun_out/gpu_tests_n2.log
+timeout -s KILL 300 python tools/congestion_real.py > gpurun_out/congestion_real.log 2>&1
+timeout -s KILL 300 python tools/staged_synth_bench.py --reps 3 > gpurun_out/staged_synth.log 2>&1
+timeout -s KILL 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29536 bench.py --gpus 2 --steps 10 --warmup 3 > gpurun_out/bench_n2.json 2> gpurun_out/bench_n2.err
+grep -E "passed|failed|FAILED|rc=" gpurun_out/gpu_tests_n2.log | tail -5
+python -c "import json; d=json.load(open('gpurun_out/congestion_real.json')); print(d['congested'], d['telemetry_over_rr'], d['telemetry_over_striping'])"
+tail -2 gpurun_out/staged_synth.log | cut -c1-400
+python -c "import json; d=json.loads(open('gpurun_out/bench_n2.json').read().strip().splitlines()[-1]); print(d['value'], d['ms_per_step'], d['e2e']['value'], d['nvlink']['elephant']['aggregate_gbs'])"
