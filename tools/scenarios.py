@@ -17,8 +17,10 @@ bandwidths and must learn the rest, as in the reference.
             +-10% window noise of 4 submitters trips; `dip_contiguous_ms` counts the windows
             that stay below from the fault on),
             a.r0 back to healthy within one probe period (1 s) + 10 ms of the recovery.
+  tiered    criterion 4: 1 direct, 3 same-socket, 4 cross-socket rails per node; the tier-1
+            share of the bytes at 64 MiB blocks (target 40-60%) and 64 KiB blocks (> 95%).
 
-Usage: python tools/scenarios.py [skewed8] [timeline] [--rate-gbs 10]"""
+Usage: python tools/scenarios.py [skewed8] [tiered] [timeline] [--rate-gbs 10]"""
 import argparse
 import json
 import os
@@ -34,7 +36,7 @@ import paper_2604_00368_b200 as sp  # noqa: E402
 from paper_2604_00368_b200 import fabrics  # noqa: E402
 
 ap = argparse.ArgumentParser()
-ap.add_argument("which", nargs="*", default=["skewed8", "timeline"])
+ap.add_argument("which", nargs="*", default=["skewed8", "tiered", "timeline"])
 ap.add_argument("--rate-gbs", type=float, default=10.0, help="declared rail bandwidth B (GB/s)")
 args = ap.parse_args()
 B = args.rate_gbs * 1e9
@@ -134,6 +136,38 @@ if "skewed8" in args.which:
     res["reference_targets"] = {"throughput_ratio": ">= 1.2", "p99_ratio": "<= 0.6", "reference_kat": "2.248x"}
     out["skewed8"] = res
     print("skewed8", json.dumps(res), flush=True)
+
+if "tiered" in args.which:
+    # criterion 4 (acceptance.cpp:241-262): per node one direct rail, three same-socket and
+    # four cross-socket rails, all at B. The sim's per-rail latencies (5 / 15 / 40 us,
+    # bench.cpp:452-470) become JITTER faults with twice that bound (uniform, same mean);
+    # its rare same-socket spikes are not emulated. One submitter thread, as the reference.
+    aff = ["direct", "same_socket", "same_socket", "same_socket"] + ["cross_socket"] * 4
+    topo = fabrics.two_node(8, B, backend="cuda", affinities=aff)
+    lat_us = [5.0, 15.0, 15.0, 15.0, 40.0, 40.0, 40.0, 40.0]
+    res = {}
+    for blk, iters in ((64 << 20, 16), (64 << 10, 64)):
+        cfg = {"resilience": {"degradation_ratio": 1e9, "degradation_events": 1 << 20}, "b200": {"chunk_bytes": 1 << 20}}
+        e = sp.Engine(topo, json.dumps(cfg), 0)
+        e.start()
+        limit_rates(e)
+        for node in ("a", "b"):
+            for i in range(8):
+                e.inject_fault(f"{node}.r{i}", sp.FaultEffect.JITTER, 0, FAR, jitter_us=2 * lat_us[i])
+        src, dst = segments(e, 8 * blk)
+        submitters(e, blk, 1, iters=2)
+        before = {e.rail_id(r): e.rail_stats(r).bytes_ok for r in range(e.rail_count())}
+        lat, moved, wall = submitters(e, blk, 1, iters=iters)
+        by = {e.rail_id(r): e.rail_stats(r).bytes_ok - before[e.rail_id(r)] for r in range(e.rail_count())}
+        a_tot = sum(v for k, v in by.items() if k.startswith("a."))
+        res[f"{blk >> 10}KiB"] = {"tier1_share": round(by["a.r0"] / max(1, a_tot), 4),
+                                  "cross_socket_share": round(sum(by[f"a.r{i}"] for i in range(4, 8)) / max(1, a_tot), 4),
+                                  "gbs": round(moved / wall / 1e9, 3)}
+        e.stop()
+        del e
+    res["reference_targets"] = {"64MiB_tier1_share": "0.40-0.60", "64KiB_tier1_share": "> 0.95"}
+    out["tiered"] = res
+    print("tiered", json.dumps(res), flush=True)
 
 if "timeline" in args.which:
     blk = 64 << 20
