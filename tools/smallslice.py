@@ -64,6 +64,9 @@ for rails in (1, 2, 4):
                             "handback_cyc_per_blk": round(dy[5] / max(1, dy[4]), 1),
                             "scalar_blocks": dy[4], "scalar_decisions": dy[3], "warp_decisions": dy[6]}
         dz = d["dz"]
+        row["dec_extra_cyc_per_blk"] = {"cand_eval_slots_dq": round(dz[3] / max(1, dy[4] or 1), 1),
+                                        "tail_records": round(dz[4] / max(1, dy[4] or 1), 1),
+                                        "slot_reserve_load_set": round(dz[5] / max(1, dy[4] or 1), 1)}
         row["fb_split"] = {"chain_cyc_per_completion": round(dz[0] / max(1, dz[1]), 1), "completions": dz[1],
                            "entries": dz[2], "busy_cyc_per_completion": round(d["fb_busy"] / max(1, dz[1]), 1)}
         print(json.dumps(row), flush=True)
