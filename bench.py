@@ -724,7 +724,7 @@ def run_b200(args):
         except Exception:
             pass
         traffic = None
-        prof = os.path.join(ROOT, "profiles", "ncu_engine_kernel_r02b.json")
+        prof = os.path.join(ROOT, "profiles", "ncu_engine_kernel_r02c.json")
         if not os.path.exists(prof):
             prof = os.path.join(ROOT, "profiles", "ncu_engine_kernel_final_r01.json")
         if os.path.exists(prof):

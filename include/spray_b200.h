@@ -189,7 +189,13 @@ int spray_inject_fault_entry(spray_engine* e, const spray_fault_entry* entry);
 int spray_clear_faults(spray_engine* e);
 uint64_t spray_engine_now_ns(spray_engine* e);
 
-/* Diagnostic snapshot (ring positions, kernel state, counters, stream status). */
+/* Diagnostic snapshot (ring positions, kernel state, counters, stream status). Word map
+ * (engine.cpp Engine::debug_words): 0-16 host/ring positions, state, device clock, byte
+ * counters, trace count, stream status, scheduler loop counters; 17-32 STATE phase clocks;
+ * 33-36 CE / completion ring positions; 37-44 per-launch timeline; 45-60 diagnostic words
+ * (b200.diag: relay tickets, host-staged drain and forwarder timings); 61 launch
+ * generation; 62-69 pipeline stage stamps; 70-77 copy-warp stamps; 78-85 decision-phase
+ * split; 86-93 FEEDBACK chain and decision-path counters; 94-101 STATE sub-step stamps. */
 int spray_engine_debug(spray_engine* e, uint64_t* out, size_t n);
 
 /* Heal timing of the most recent DOWN fault: fault start -> first retried slice OK,
