@@ -1213,11 +1213,16 @@ uint64_t Engine::allocate_batch() {
 
 uint64_t Engine::allocate_batch_locked() {
   if (!started_) throw EngineError("engine not started");
-  for (uint32_t k = 0; k < opts_.batch_slots; ++k) {
-    const uint32_t slot = (next_slot_ + k) % opts_.batch_slots;
+  // the slot of the batch freed last (if it completed) first: its delivered counter is
+  // still in the scheduler's counter cache, so the batch's first completion does not wait
+  // on an HBM read of a cold slot; otherwise round robin
+  const int64_t hint = last_freed_;
+  last_freed_ = -1;
+  for (uint32_t k = 0; k <= opts_.batch_slots; ++k) {
+    const uint32_t slot = (hint >= 0 && k == 0) ? static_cast<uint32_t>(hint) : (next_slot_ + k) % opts_.batch_slots;
     if (slot_busy_[slot]) continue;
     slot_busy_[slot] = 1;
-    next_slot_ = slot + 1;
+    if (!(hint >= 0 && k == 0)) next_slot_ = slot + 1;
     BatchRec b;
     b.id = next_batch_++;
     b.slot = slot;
@@ -1275,6 +1280,7 @@ void Engine::free_batch_locked(uint64_t batch) {
   const uint64_t done = m->done - b.base;
   if (!failed && b.submitted > 0 && done < b.submitted) throw EngineError("cannot free an in-flight batch");
   slot_busy_[b.slot] = 0;
+  if (!failed) last_freed_ = b.slot;  // a failed batch's slot may still see late completions
   batches_.erase(batch);
 }
 

@@ -180,6 +180,7 @@ class Engine {
   std::vector<uint8_t> slot_busy_;
   uint64_t next_batch_ = 1, next_transfer_ = 1;
   uint32_t next_slot_ = 0;
+  int64_t last_freed_ = -1;  // slot of the last batch freed after completing (allocated first)
   std::map<std::string, uint32_t> set_cache_;
   std::vector<std::vector<LocalCandidate>> sets_;
   bool started_ = false;
