@@ -681,6 +681,8 @@ void Engine::free_device() {
     for (void* p : kv.second.registered) cudaHostUnregister(p);
   if (board_registered_) cudaHostUnregister(board_registered_), board_registered_ = nullptr;
   if (hold_) cudaFreeHost(const_cast<uint32_t*>(hold_)), hold_ = nullptr, hold_dev_ = nullptr;
+  if (stage_host_) cudaFreeHost(stage_host_), stage_host_ = nullptr;
+  for (auto& d : stage_dev_) d = nullptr;  // freed with dev_allocs_
   for (auto& s : ce_streams_)
     if (s) cudaStreamDestroy(s);
   ce_streams_.clear();
@@ -1385,6 +1387,7 @@ uint64_t Engine::submit_transfer(uint64_t batch, const spray_transfer_request& r
 // a large batch while the host is still translating its tail (order is unchanged).
 size_t Engine::submit_transfers(uint64_t batch, const spray_transfer_request* reqs, size_t n, uint64_t* ids) {
   std::lock_guard<std::mutex> lk(mu_);
+  if (n >= kStageMin) return submit_staged_locked(batch, reqs, n, ids);
   constexpr size_t kGroup = 256;
   Intent v[kGroup];
   size_t nv = 0, done = 0;
@@ -1405,6 +1408,79 @@ size_t Engine::submit_transfers(uint64_t batch, const spray_transfer_request* re
     throw;
   }
   if (nv) publish(v, nv);
+  return done;
+}
+
+// A large submission goes to the device as bulk intent arrays in HBM (one copy-engine copy
+// and one ring entry per kStageCap intents, so the device starts on the first piece while
+// the host builds the next) instead of through the mapped ring: the
+// HOSTRX warp's reads of host memory queue behind every write the engine has posted to the
+// PCIe root, so under a host-bound batch the ring is fetched at the pace of that backlog.
+// kStageAreas device areas rotate; an area is refilled only after INGRESS has finished the bulk
+// array it last held (the device's bulk_done counter). Order and accounting are those of
+// the ring path.
+size_t Engine::submit_staged_locked(uint64_t batch, const spray_transfer_request* reqs, size_t n, uint64_t* ids) {
+  CK(cudaSetDevice(device_));
+  if (!stage_host_) {
+    void* h = nullptr;
+    CK(cudaHostAlloc(&h, sizeof(Intent) * kStageCap * kStageAreas, cudaHostAllocPortable));
+    stage_host_ = static_cast<Intent*>(h);
+    for (Intent*& d : stage_dev_) {
+      void* p = nullptr;
+      CK(cudaMalloc(&p, sizeof(Intent) * kStageCap));
+      dev_allocs_.push_back(p);
+      d = static_cast<Intent*>(p);
+    }
+  }
+  LookupCache lc;
+  size_t done = 0;
+  for (uint32_t piece = 0; done < n; ++piece) {
+    const size_t k = std::min(kStageCap, n - done);
+    const uint32_t a = static_cast<uint32_t>(bulk_pub_ % kStageAreas);
+    Intent* hs = stage_host_ + size_t(a) * kStageCap;
+    const auto t0 = std::chrono::steady_clock::now();
+    while (stage_use_[a] && ctl_->bulk_done < stage_use_[a]) {  // INGRESS still reads it
+      ensure_running();
+      if (std::chrono::steady_clock::now() - t0 > std::chrono::seconds(60))
+        throw EngineError("staged submit: bulk array not consumed within 60 s");
+      _mm_pause();
+    }
+    size_t built = 0;
+    try {
+      for (; built < k; ++built) {
+        uint64_t sl = 0;
+        hs[built] = make_intent(batch, reqs[done + built], &sl, &lc);
+        lc.batch->submitted += sl;
+        if (ids) ids[done + built] = hs[built].transfer_id;
+      }
+    } catch (...) {
+      // what was built so far still goes out, as the ring path would have published it
+      if (built) {
+        CK(cudaMemcpyAsync(stage_dev_[a], hs, sizeof(Intent) * built, cudaMemcpyHostToDevice, copy_stream_));
+        CK(cudaStreamSynchronize(copy_stream_));
+        Intent bulk{};
+        bulk.batch_id = lc.batch->id;
+        bulk.src = reinterpret_cast<uint64_t>(stage_dev_[a]);
+        bulk.len = built;
+        bulk.batch_slot = lc.batch->slot;
+        bulk.flags = kIntentBulk;
+        stage_use_[a] = ++bulk_pub_;
+        publish(&bulk, 1);
+      }
+      throw;
+    }
+    CK(cudaMemcpyAsync(stage_dev_[a], hs, sizeof(Intent) * k, cudaMemcpyHostToDevice, copy_stream_));
+    CK(cudaStreamSynchronize(copy_stream_));
+    Intent bulk{};
+    bulk.batch_id = lc.batch->id;
+    bulk.src = reinterpret_cast<uint64_t>(stage_dev_[a]);
+    bulk.len = k;
+    bulk.batch_slot = lc.batch->slot;
+    bulk.flags = kIntentBulk;
+    stage_use_[a] = ++bulk_pub_;
+    publish(&bulk, 1);
+    done += k;
+  }
   return done;
 }
 
@@ -1441,6 +1517,7 @@ void Engine::submit_device_intents(uint64_t batch, const void* dev_intents, uint
   bulk.len = n;
   bulk.batch_slot = b.slot;
   bulk.flags = kIntentBulk;
+  ++bulk_pub_;
   publish(&bulk, 1);
 }
 
@@ -1459,6 +1536,7 @@ float Engine::run_device_intents_timed(uint64_t batch, const void* dev_intents, 
   bulk.len = n;
   bulk.batch_slot = b.slot;
   bulk.flags = kIntentBulk;
+  ++bulk_pub_;
   ring_[sub_tail_ % opts_.sub_capacity] = bulk;
   ++sub_tail_;
   std::atomic_thread_fence(std::memory_order_release);

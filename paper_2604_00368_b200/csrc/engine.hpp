@@ -219,6 +219,14 @@ class Engine {
   void* board_registered_ = nullptr;  // host board this engine registered (unregistered on free)
   volatile uint32_t* hold_ = nullptr;  // mapped flag of the timed-run stream hold
   uint32_t* hold_dev_ = nullptr;
+  // large submissions are staged through HBM as bulk intent arrays (submit_staged_locked)
+  static constexpr size_t kStageMin = 1024, kStageCap = 1024;  // intents (per piece / area)
+  static constexpr uint32_t kStageAreas = 8;
+  spray_dev::Intent* stage_host_ = nullptr;      // pinned, kStageAreas x kStageCap intents
+  spray_dev::Intent* stage_dev_[kStageAreas] = {};
+  uint64_t stage_use_[kStageAreas] = {};  // bulk index of each area's last use (1-based)
+  uint64_t bulk_pub_ = 0;             // bulk entries this engine has published
+  size_t submit_staged_locked(uint64_t batch, const spray_transfer_request* reqs, size_t n, uint64_t* ids);
   uint32_t launch_gen_ = 0;
   void setup_relay(uint32_t idx, int via, bool host_staged);
   void sync_relays();
