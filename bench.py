@@ -9,8 +9,9 @@ runs its own batch over its own PCIe root (weak scaling, no data-path collective
 
   value    device-resident intents (prepared once in HBM), engine kernel launched in
            drain mode and timed with CUDA events on its stream: GB/s delivered.
-  e2e      the public C-ABI path from host arrays: submit_transfers (8192 intents through
-           the mapped submission ring) + await_batch, wall clock, CUDA-synchronised.
+  e2e      the public C-ABI path from host arrays: submit_transfers (8192 intents; the
+           engine stages them to HBM as bulk arrays, 1024 per copy-engine copy, inside the
+           timed region) + await_batch, wall clock.
   roofline the engine kernel against PCIe Gen5 x16 full duplex.
   cpu_baseline  the reference's own CPU engine (oracle/_ref, unmodified reference sources)
            on this host: memory backend, real clock, same block batch, one direction.
