@@ -398,6 +398,45 @@ def test_batch_api_semantics():
     e.stop()
 
 
+@pytest.mark.parametrize("bad_at", [None, 1500, 2047])
+def test_large_submission_staged_through_hbm(bad_at):
+    """submit_transfers with >= 1024 requests goes to the device as bulk intent arrays
+    (1024 per copy, rotating HBM areas): bytes, ids and batch accounting as one by one,
+    across several submissions that reuse the areas; an invalid request raises after the
+    requests before it were submitted, exactly as the ring path does."""
+    topo = fabrics.two_node(2, 1e9, backend="cuda")
+    e = make_engine(topo, {"b200": {"chunk_bytes": 65536}})
+    blk, nb = 16 << 10, 3000
+    n = blk * nb
+    s, d = dev_buf(n, 31), dev_buf(n)
+    e.register_segment(sp.SegmentDescriptor("s", sp.Medium.DEVICE, "a", [sp.BufferDesc(0, n, s.data_ptr())]))
+    e.register_segment(sp.SegmentDescriptor("d", sp.Medium.DEVICE, "b", [sp.BufferDesc(0, n, d.data_ptr())]))
+    perm = np.random.default_rng(5).permutation(nb)
+    for rep in range(3):  # 3 x 3 pieces: every staging area is reused
+        d.zero_()
+        torch.cuda.synchronize()
+        reqs = [sp.TransferRequest("s", i * blk, "d", int(perm[i]) * blk, blk) for i in range(nb)]
+        if bad_at is not None:
+            reqs[bad_at] = sp.TransferRequest("s", n - 10, "d", 0, 20)  # out of range
+        b = e.allocate_batch()
+        if bad_at is None:
+            e.submit_transfers(b, reqs)
+            upto = nb
+        else:
+            with pytest.raises(sp.InvalidRangeError):
+                e.submit_transfers(b, reqs)
+            upto = bad_at
+        st = e.await_batch(b, 30_000_000_000)
+        assert st.state == sp.BatchState.COMPLETE and st.remaining == 0
+        e.free_batch(b)
+        src_v, dst_v = s.view(nb, blk), d.view(nb, blk)
+        idx = torch.as_tensor(perm[:upto])
+        assert torch.equal(dst_v[idx], src_v[:upto])
+        if upto < nb:
+            assert not dst_v[torch.as_tensor(perm[upto:])].any()
+    e.stop()
+
+
 # ------------------------------------------------------------------ self-healing
 @pytest.mark.parametrize("policy", ["telemetry", "rr", "hash"])
 def test_down_fault_reroutes_with_zero_lost_bytes(co, policy):
